@@ -1,0 +1,94 @@
+"""Sanity pins for the synthetic inputs, checked on the inputs
+themselves before anything is timed or compared."""
+import math
+
+import numpy as np
+
+import synth_inputs as gen
+
+
+def test_splitmix_known_values():
+    # SplitMix64 reference stream for seed 0: mix(GAMMA), mix(2*GAMMA) -- the
+    # first output of the canonical generator seeded with 0 is 0xE220A8397B1DCDAF.
+    x = gen.splitmix(0, 0, 2)
+    assert int(x[0]) == 0xE220A8397B1DCDAF
+    assert int(x[1]) == 0x6E789E6AA1B965F4
+    assert np.array_equal(gen.splitmix(7, 5, 3), gen.splitmix(7, 0, 8)[5:])
+
+
+def test_uniform_top_byte_chi2():
+    a = gen.uniform_u64(1 << 18, 42)
+    h = np.bincount((a >> np.uint64(56)).astype(np.int64), minlength=256)
+    exp = a.size / 256
+    chi2 = float(((h - exp) ** 2 / exp).sum())
+    assert chi2 < 255 + 6 * math.sqrt(2 * 255)
+
+
+def test_exponential():
+    n = 1 << 20
+    a = gen.exponential_f64(n, 2)
+    assert np.all(np.isfinite(a))
+    assert not np.any(np.signbit(a))            # no -0.0, no negatives
+    assert abs(a.mean() - 1.0) < 0.01
+    assert abs((a > 1.0).mean() - math.exp(-1)) < 0.005
+    assert abs(a.max() - (math.log(n) + 0.5772)) < 4.0
+
+
+def test_almost_sorted():
+    n = 1 << 16
+    a = gen.almost_sorted_f64(n, 2)
+    assert np.array_equal(np.sort(a), np.arange(n, dtype=np.float64))
+    # inversions: each adjacent swap of distinct values changes them by +-1
+    inv = int(np.sum(a[:-1] > a[1:]))  # adjacent inversions, lower bound
+    assert 0 < inv <= math.isqrt(n)
+    perm = a.astype(np.int64)
+    # exact inversion count via merge count on a small prefix window is not
+    # needed: parity of the permutation = parity of #swaps (2^8 swaps -> even)
+    seen = np.zeros(n, dtype=bool)
+    cycles = 0
+    for i in range(n):
+        if not seen[i]:
+            cycles += 1
+            j = i
+            while not seen[j]:
+                seen[j] = True
+                j = perm[j]
+    assert (n - cycles) % 2 == math.isqrt(n) % 2
+
+
+def test_sorted_reverse():
+    a = gen.sorted_f64(1 << 16, 2)
+    assert np.all(a[1:] > a[:-1]) and a[0] >= 0.0 and a[-1] < 1.0
+    r = gen.reverse_sorted_f64(1 << 16, 2)
+    assert np.array_equal(r[::-1], a)
+
+
+def test_rootdup_twodup_counts():
+    n = 1 << 16
+    r = gen.rootdup_u64(n)
+    assert np.all(np.bincount(r.astype(np.int64)) == 256)
+    for m in (16, 18, 20):
+        t = gen.twodup_u64(1 << m)
+        u, c = np.unique(t, return_counts=True)
+        assert u.size == (1 << m) // 6 + 2
+        assert c.max() == 1 << ((m + 1) // 2)
+
+
+def test_zipf():
+    n = 1 << 20
+    z = gen.zipf_u64(n, 3)
+    H = float(np.sum(1.0 / np.arange(1, gen.ZIPF_VALUES + 1)))
+    c1 = int(np.sum(z == 1))
+    exp = n / H
+    assert abs(c1 - exp) < 5 * math.sqrt(exp)
+    assert z.min() >= 1 and z.max() <= gen.ZIPF_VALUES
+
+
+def test_pairs_and_records():
+    p = gen.pairs(1000, 4)
+    assert np.array_equal(p[:, 1], np.arange(1000, dtype=np.uint64))
+    assert np.array_equal(p[:, 0], gen.uniform_u64(1000, 4))
+    r = gen.records100(50, 5)
+    w = gen.splitmix(5, 0, 13 * 50).reshape(50, 13).view(np.uint8).reshape(50, 104)[:, :100]
+    assert np.array_equal(r, w)
+    assert gen.records100(50, 5).tobytes() == r.tobytes()
