@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: Gkeys/s of the in-place IPS4o sort of 2^30 uint64 Uniform keys
+on B200 (BASELINE.json metric), plus the HBM roofline of the dominant kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n LOG2N] [--dist uniform_u64] [--algo tree|digit]
+
+One step = one full ips4o_sort of the whole array (all SURVEY 8(a) rows:
+pre-pass, sampling, classification, boundaries, stripe fix, permutation,
+cleanup, scheduling, base case) on inputs already resident in HBM.  Before
+every step (outside the timed region) the working array is restored from a
+pristine device copy; the 8 GiB input is far larger than the 126 MB L2, so no
+extra L2 flush is needed.  Timing: CUDA events on the sorting stream,
+bracketed by barrier + synchronize; max over ranks.  N > 1 runs independent
+replicas (DESIGN "Multi-GPU: replicas only"), weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DTYPES = {"u64": 0, "f64": 1, "pair": 2, "rec100": 3}
+ELEM = {0: 8, 1: 8, 2: 16, 3: 100}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=30, help="log2 of the element count")
+    ap.add_argument("--dist", default="uniform_u64")
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--algo", default="tree", choices=["tree", "digit"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-log2", type=int, default=25, help="oracle sample size (log2)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        time.sleep(0.05)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+def make_input(dist: str, n: int, seed: int):
+    import numpy as np
+
+    import synth_inputs as gen
+
+    a = gen.generate(dist, n, seed)
+    return np.ascontiguousarray(a)
+
+
+def cpu_baseline(dist: str, log2n: int, seed: int) -> dict:
+    """The oracle as it stands (single-threaded C mergesort) on a bounded
+    sample of the same workload: the first 2^log2n keys of the same stream."""
+    import oracle
+
+    n = 1 << log2n
+    a = make_input(dist, n, seed)
+    dt = {"f64": 1, "pair": 2, "rec100": 3}.get(dist.split("_")[-1], 0)
+    if dist == "pairs":
+        dt = 2
+    if dist == "records100":
+        dt = 3
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.sort_inplace(a, dt)
+    t = time.perf_counter() - t0
+    return {"value": n / t / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+            "sample": f"first 2^{log2n} keys of the {dist} stream (seed {seed}), "
+                      f"single-threaded top-down mergesort, {t:.2f} s",
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def dist_dtype(dist: str) -> int:
+    return {"pairs": 2, "records100": 3}.get(dist, 1 if dist.endswith("_f64") else 0)
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    dt = dist_dtype(args.dist)
+    log2 = min(args.cpu_log2 - 2, args.n)   # per step: a bounded sample
+    n = 1 << log2
+    a = make_input(args.dist, n, args.seed)
+    times = []
+    for i in range(args.warmup + args.steps):
+        b = a.copy()
+        t0 = time.perf_counter()
+        oracle.sort_inplace(b, dt)
+        t = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(t)
+    tot = sum(times)
+    val = n * len(times) / tot / 1e9
+    line = {
+        "impl": "reference", "metric": "Gkeys/s sorted in place, 2^30 uint64 Uniform; HBM GB/s per partition pass",
+        "value": val, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64" if dt == 0 else ["u64", "f64", "pair", "rec100"][dt],
+        "data": "synthetic",
+        "config": {"workload": f"{args.dist} n=2^{args.n} (reference arm: oracle on a 2^{log2} sample per step)",
+                   "n": 1 << args.n, "seed": args.seed},
+        "cpu_baseline": {"value": val, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first 2^{log2} keys of the {args.dist} stream per step",
+                         "host_cpu": _cpu_model()},
+        "e2e": {"value": val, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+
+    import paper_2009_13569_b200 as ips
+    from paper_2009_13569_b200 import build
+
+    build.build()
+    ips.load()
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dt = dist_dtype(args.dist)
+    D = ELEM[dt]
+    n = 1 << args.n
+    algo = ips.DIGIT if args.algo == "digit" else ips.TREE
+    host = make_input(args.dist, n, args.seed + rank)
+    hbytes = np.ascontiguousarray(host).view(np.uint8).reshape(-1)
+    pristine = torch.empty(n * D, dtype=torch.uint8, device=dev)
+    pristine.copy_(torch.from_numpy(hbytes))
+    work = torch.empty_like(pristine)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(stats: bool):
+        work.copy_(pristine)
+        torch.cuda.synchronize(dev)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        st = ips.sort_ex(work, dt, algo=algo, timing=True) if stats else ips.sort(work, dt, algo=algo)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        return ev0.elapsed_time(ev1), st
+
+    for _ in range(args.warmup):
+        one_step(False)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = ClockSampler(local_rank)
+    clk.start()
+    times, stats = [], []
+    for _ in range(args.steps):
+        t, st = one_step(True)
+        times.append(t)
+        stats.append(st)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    total_ms = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        dist.barrier()
+    # correctness guard on the last result (cheap, on device): non-decreasing
+    chk_ok = None
+    if dt == 0:
+        w = work.view(torch.int64)
+        # unsigned compare via xor of the sign bit
+        s = w ^ torch.tensor(-(2**63), dtype=torch.int64, device=dev)
+        chk_ok = bool((s[1:] >= s[:-1]).all().item())
+    if rank != 0:
+        return
+    value = world * n * args.steps / (total_ms / 1e3) / 1e9
+    st = stats[-1]
+    km = {k: statistics.mean(s["kernel_ms"][k] for s in stats) for k in stats[0]["kernel_ms"]}
+    # roofline of the dominant kernel family
+    elems_levels = sum(st["elems_per_level"])
+    alg = {
+        "classify": 2 * D * elems_levels,
+        "permute": 2 * D * elems_levels,
+        "basecase": 2 * D * st["basecase_elems"],
+        "prepass": D * n,
+    }
+    fams = {k: km[k] for k in alg if km.get(k, 0) > 0}
+    dom = max(fams, key=fams.get) if fams else "classify"
+    peak, peak_src = peaks()
+    achieved = alg[dom] / (km[dom] / 1e3) / 1e9 if km.get(dom) else None
+    traffic = ncu_traffic()
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak if achieved else None,
+            "traffic": (traffic or {}).get(dom), "peak_source": peak_src,
+            "alg_bytes_per_step": alg[dom], "kernel_ms_per_step": km[dom]}
+    # algorithmic whole-sort reading: 2 n D per partition level (+ base case)
+    L_eff = elems_levels / n
+    sort_ms = total_ms / args.steps
+    roof_sort = {"levels_eff": L_eff,
+                 "frac_partition_2nDL": (2 * n * D * L_eff / (peak * 1e9)) / (
+                     (km["classify"] + km["permute"] + km["stripe_fix"] + km["cleanup"] + km["sample"]
+                      + km["boundaries"] + km["schedule"]) / 1e3) if L_eff else None,
+                 "frac_sort_2nD_L_plus_1": (2 * n * D * (L_eff + 1) / (peak * 1e9)) / (sort_ms / 1e3)}
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        pin = torch.empty(n * D, dtype=torch.uint8).pin_memory()
+        src = torch.from_numpy(hbytes)
+        et = []
+        for i in range(args.e2e_steps + 1):
+            pin.copy_(src)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ips.sort_host(pin, dt, algo=algo)
+            t1 = time.perf_counter()
+            if i > 0:
+                et.append(t1 - t0)
+        e2e = {"value": n * len(et) / sum(et) / 1e9, "unit": "Gkeys/s",
+               "h2d_bytes_per_step": n * D, "d2h_bytes_per_step": n * D,
+               "path": "ips4o_sort_host (pinned host buffer; H2D + sort + D2H inside the call)"}
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline(args.dist, min(args.cpu_log2, args.n), args.seed)
+    line = {
+        "metric": "Gkeys/s sorted in place, 2^30 uint64 Uniform; HBM GB/s per partition pass",
+        "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": ["u64", "f64", "pair", "rec100"][dt], "data": "synthetic",
+        "config": {"workload": f"{args.dist} n=2^{args.n} ({'IPS4o tree' if algo == 0 else 'IPS2Ra digit'})",
+                   "n_per_gpu": n, "seed": args.seed, "algo": args.algo,
+                   "l2": "inputs (8 GiB) larger than L2; working array restored from a pristine copy "
+                         "before each step, outside the timed region",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": roof, "roofline_sort": roof_sort,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "kernel_ms_per_step": km, "levels": st["levels"], "tasks_per_level": st["tasks_per_level"],
+        "basecase_tasks": st["basecase_tasks"], "scratch_bytes": st["scratch_bytes"],
+        "sorted_check": chk_ok, "step_ms": times,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

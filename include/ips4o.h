@@ -1,0 +1,196 @@
+/*
+ * ips4o.h -- C ABI of the B200-native in-place samplesort partitioning step
+ * (IPS4o, with the IPS2Ra radix classifier) from Axtmann, Witt, Ferizovic,
+ * Sanders, "Engineering In-place (Shared-memory) Sorting Algorithms",
+ * arXiv 2009.13569.  Citations "P:<line>" refer to the paper's LaTeX source
+ * (PAPER.md line, section named next to it).
+ *
+ * Problem statement (Sec. 2): the input is an array A[0..n-1] of n
+ * elements and the output is stored in the input array.  "In-place" means
+ * sub-linear additional space; here the auxiliary DEVICE memory is
+ * O(k*b) per CTA plus O(#tasks) task records, reported by
+ * ips4o_scratch_bytes() and ips4o_stats.scratch_bytes.
+ *
+ * All entry points are plain C: raw pointers, sizes, and a cudaStream_t passed
+ * as void*.  No PyTorch or C++ types cross this boundary.  Every call returns
+ * an int status (0 = success, negative = IPS4O_ERR_*) and never throws.
+ */
+#ifndef IPS4O_H
+#define IPS4O_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- element types
+ * P:1877-1886 (data types of the experiments) and Alg. 3/4.
+ *   IPS4O_U64           8 B, unsigned 64-bit key, ascending unsigned order.
+ *   IPS4O_F64           8 B IEEE-754 double, ascending '<'.  Precondition: no
+ *                       NaN; if both -0.0 and +0.0 occur their relative order
+ *                       is unspecified (-0.0 sorts first).
+ *   IPS4O_PAIR_U64_U64  16 B {uint64 key; uint64 value}, ordered by key only.
+ *   IPS4O_REC100_KEY10  100 B record, key = bytes 0..9 compared
+ *                       lexicographically as unsigned bytes (Alg. 4), payload
+ *                       bytes 10..99 carried along.
+ * The sort is NOT stable (the block permutation P:840-922 moves whole blocks
+ * in arbitrary order; DESIGN R3): for PAIR and REC100 the order inside a run
+ * of equal keys is unspecified. */
+enum ips4o_dtype {
+    IPS4O_U64 = 0,
+    IPS4O_F64 = 1,
+    IPS4O_PAIR_U64_U64 = 2,
+    IPS4O_REC100_KEY10 = 3
+};
+
+/* Classifier of the partitioning step. */
+enum ips4o_algo {
+    IPS4O_ALGO_TREE = 0,  /* IPS4o: sample + branchless splitter tree with
+                             equality buckets        */
+    IPS4O_ALGO_DIGIT = 1  /* IPS2Ra: MSB digit extractor     */
+};
+
+/* Status codes. */
+enum ips4o_status {
+    IPS4O_OK = 0,
+    IPS4O_ERR_INVALID = -1, /* NULL ptr with n > 0, unknown dtype/algo, misaligned
+                               ptr (needs 16-byte alignment), n >= 2^32, bad option */
+    IPS4O_ERR_NOMEM = -2,   /* device scratch (or pinned host) allocation failed  */
+    IPS4O_ERR_CUDA = -3,    /* a CUDA launch or runtime call failed; the CUDA error
+                               string is kept for ips4o_status_string()           */
+    IPS4O_ERR_NOGPU = -4    /* no CUDA device / device is not sm_100             */
+};
+
+/* Options of ips4o_sort_ex (NULL = defaults).  Zero in a field = default. */
+typedef struct ips4o_options {
+    int32_t algo;          /* enum ips4o_algo (default TREE)                          */
+    int32_t k_max;         /* max leaves/digits per partitioning step (k=256),
+                              power of two in [2, 256]; default per dtype            */
+    uint64_t seed;         /* sampling seed (DESIGN R8); default 0x1F4A2C7            */
+    int32_t alpha_min;     /* lower bound of the oversampling factor alpha; the paper
+                              uses alpha = 0.2 log2 n, default max(that, 32) */
+    int32_t base_cap;      /* base-case capacity M (elements per one-CTA sort);
+                              default and maximum per dtype (DESIGN "Base case")      */
+    int32_t max_levels;    /* stop after this many partitioning levels (debug);
+                              0 = unlimited.  With a limit the array is PARTITIONED,
+                              not sorted, unless all buckets reached the base case.  */
+    int32_t skip_prepass;  /* 1 = do not run the easy-input pre-pass   */
+    int32_t skip_basecase; /* 1 = do not run the base case (debug; leaves buckets
+                              unsorted)                                               */
+    int32_t timing;        /* 1 = record per-kernel device times into ips4o_stats     */
+    int32_t reserved[7];
+} ips4o_options;
+
+#define IPS4O_MAX_LEVELS_REPORTED 16
+#define IPS4O_NUM_KERNELS 12
+
+/* Statistics (optional output of ips4o_sort_ex; a non-NULL pointer implies a
+ * stream synchronisation before return). */
+typedef struct ips4o_stats {
+    uint64_t scratch_bytes;           /* peak device scratch of this call             */
+    int32_t levels;                   /* partitioning levels executed                 */
+    int32_t easy_input;               /* 0 none, 1 sorted, 2 reverse-sorted (reversed),
+                                         3 all keys equal                             */
+    uint64_t tasks_per_level[IPS4O_MAX_LEVELS_REPORTED];
+    uint64_t elems_per_level[IPS4O_MAX_LEVELS_REPORTED]; /* sum of task sizes      */
+    uint64_t basecase_tasks;          /* number of one-CTA base-case sorts            */
+    uint64_t basecase_elems;          /* elements sorted by the base case             */
+    uint64_t equal_elems;             /* elements left in terminal equality buckets   */
+    float kernel_ms[IPS4O_NUM_KERNELS]; /* per kernel family, when opt->timing:
+                                         0 prepass, 1 sample, 2 classify, 3 boundaries,
+                                         4 stripe-fix, 5 permute, 6 cleanup, 7 schedule,
+                                         8 base case, 9 reverse, 10 host planning (wall),
+                                         11 total (device)                            */
+    uint64_t kernel_launches;         /* kernels launched by this call                */
+} ips4o_stats;
+
+/* Sort the n elements at DEVICE pointer ptr ascending, in place, unstably,
+ * stream-ordered on `stream` (a cudaStream_t, or NULL for the legacy default
+ * stream).  ptr must be 16-byte aligned (torch's allocator gives >= 256 B).
+ * The caller owns ptr and keeps it alive until the stream work completes.
+ * Scratch is allocated stream-ordered from the device's default memory pool
+ * and released before return.  The call synchronises `stream` once per
+ * partitioning level to read back the task list (DESIGN "Host loop"); from
+ * the caller's point of view it behaves like a blocking library call whose
+ * results are visible to later work on `stream`.
+ * Errors: IPS4O_ERR_INVALID, IPS4O_ERR_NOMEM, IPS4O_ERR_CUDA, IPS4O_ERR_NOGPU.
+ * n <= 1 returns 0 without device work. */
+int ips4o_sort(void *ptr, uint64_t n, int dtype, void *stream);
+
+/* As ips4o_sort with options (NULL = defaults) and optional statistics. */
+int ips4o_sort_ex(void *ptr, uint64_t n, int dtype, void *stream,
+                  const ips4o_options *opt, ips4o_stats *out);
+
+/* End-to-end call on HOST memory: copies host_ptr[0..n) to the device (through
+ * pinned staging), sorts it with ips4o_sort_ex, copies the result back into
+ * host_ptr, and synchronises.  host_ptr needs 16-byte alignment; if it is
+ * already page-locked (cudaHostAlloc/cudaHostRegister) it is used directly.
+ * Device memory for the array is allocated and freed inside the call. */
+int ips4o_sort_host(void *host_ptr, uint64_t n, int dtype,
+                    const ips4o_options *opt, ips4o_stats *out);
+
+/* Upper bound of the device scratch bytes ips4o_sort_ex may allocate for
+ * (n, dtype, opt) -- O(G*k*b*D + #tasks), "the scratch bytes are reported". */
+uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt);
+
+/* Human-readable text of a status code (for IPS4O_ERR_CUDA: the last CUDA
+ * error string seen by this thread). */
+const char *ips4o_status_string(int status);
+
+/* Per-dtype parameters the library uses (for tests and reports). */
+typedef struct ips4o_dtype_info {
+    int32_t elem_bytes;    /* D                                                      */
+    int32_t block_elems;   /* b: elements per block (DESIGN "H1")     */
+    int32_t kidx_max;      /* bucket indices per CTA (buffer blocks in shared memory)*/
+    int32_t base_cap;      /* base-case capacity M                                   */
+    int32_t key_bytes;     /* bytes of a key in ips4o_step_info arrays (8 or 16)      */
+} ips4o_dtype_info;
+int ips4o_get_dtype_info(int dtype, ips4o_dtype_info *out);
+
+/* ---------------------------------------------------------------- test hooks
+ * One partitioning step (Sec. 4.1: sampling, classification,
+ * block permutation, cleanup) over the whole array A[0..n), with NO recursion
+ * and no base case.  Afterwards A is partitioned into buckets
+ * [E[j], E[j+1]), j < num_buckets.  The classifier actually used is returned
+ * in raw KEY form (not the internal order-preserving form):
+ *   key_bytes = 8 : U64/PAIR key as uint64, F64 as the double's bit pattern;
+ *   key_bytes = 16: REC100 key bytes 0..9 followed by 6 zero bytes.
+ * tree[1..s] / splitter[0..s] with s = 2^l - 1 (tree[0] unused, zero) follow
+ * P:402-406.  For IPS4O_ALGO_DIGIT, tree/splitter are untouched and
+ * `shift`, `l` (= digit bits) describe the extractor (key >> shift) & (2^l - 1)
+ * over the order-preserving 64-bit (or 80-bit) key.
+ * Host arrays are caller-owned: E needs room for kidx_max+1 uint64,
+ * tree and splitter for kidx_max keys of key_bytes each.  Synchronous. */
+typedef struct ips4o_step_info {
+    int32_t algo;
+    int32_t num_buckets;   /* K: bucket indices (2^l, or 2^(l+1) with equality)   */
+    int32_t l;             /* log2 leaves (tree) / digit bits (radix)             */
+    int32_t equality;      /* equality buckets enabled                */
+    int32_t shift;         /* radix shift (DIGIT)                                 */
+    int32_t k_req;         /* k requested by the level planner (power of two)     */
+    int32_t k_used;        /* k after the equality budget rule (DESIGN R10)       */
+    int32_t samples;       /* m = alpha * k samples drawn (TREE)                  */
+    int32_t kidx_budget;   /* bucket-index budget of the equality rule (R10)      */
+    int32_t level;         /* sampling level argument (0 here)                    */
+    uint64_t seed;         /* seed used                                           */
+    uint64_t *E;           /* [num_buckets + 1] exact bucket boundaries (out)     */
+    void *tree;            /* [2^l] keys (out, TREE)                              */
+    void *splitter;        /* [2^l] keys (out, TREE)                              */
+} ips4o_step_info;
+int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream,
+                         const ips4o_options *opt, ips4o_step_info *info);
+
+/* Classify n elements at DEVICE pointer elems with the branchless tree of
+ * P:432-437 built from the u sorted, unique splitter keys at HOST pointer
+ * splitters (raw key form, key_bytes each); equality buckets if `equality`.
+ * Writes one uint32 bucket index per element to DEVICE pointer out.  This is
+ * the classifier the classification kernel uses (test hook).  Synchronous. */
+int ips4o_classify(const void *elems, uint64_t n, int dtype, const void *splitters,
+                   int u, int equality, uint32_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IPS4O_H */

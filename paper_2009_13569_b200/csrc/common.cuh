@@ -1,0 +1,211 @@
+// common.cuh -- per-dtype traits and small device helpers of the sm_100a path.
+// Product code; independent of oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace ips4o {
+
+// ------------------------------------------------------------------ keys
+// Keys live in an order-preserving unsigned space: comparisons are plain
+// unsigned '<'.  The element BYTES are what gets moved; the key is only used
+// to classify.
+
+__host__ __device__ __forceinline__ u64 f64_to_key(u64 bits) {
+  // negative doubles: flip all bits; non-negative: flip the sign bit
+  return bits ^ ((u64)((i64)bits >> 63) | (1ull << 63));
+}
+__host__ __device__ __forceinline__ u64 key_to_f64(u64 k) {
+  return k ^ ((u64)((i64)(~k) >> 63) | (1ull << 63));
+}
+
+__device__ __forceinline__ u32 bswap32(u32 x) { return __byte_perm(x, 0, 0x0123); }
+
+template <int DT> struct Traits;
+
+template <> struct Traits<DT_U64> {
+  static constexpr int D = 8;
+  using Key = u64;
+  using Unit = u64;                 // copy unit (element alignment)
+  static constexpr int B = 64;      // elements per block -> 512 B blocks
+  static constexpr int KIDX = 256;  // bucket indices (buffer blocks) per CTA
+  static constexpr int BASE_CAP = 24576;
+  static constexpr int CLS_THREADS = 512;
+  static constexpr int CLS_TILE = 2048;
+  static constexpr int KEY_UNITS = 1;
+  __device__ __forceinline__ static Key key(const char *e) { return *reinterpret_cast<const u64 *>(e); }
+};
+
+template <> struct Traits<DT_F64> {
+  static constexpr int D = 8;
+  using Key = u64;
+  using Unit = u64;
+  static constexpr int B = 64;
+  static constexpr int KIDX = 256;
+  static constexpr int BASE_CAP = 24576;
+  static constexpr int CLS_THREADS = 512;
+  static constexpr int CLS_TILE = 2048;
+  static constexpr int KEY_UNITS = 1;
+  __device__ __forceinline__ static Key key(const char *e) {
+    return f64_to_key(*reinterpret_cast<const u64 *>(e));
+  }
+};
+
+template <> struct Traits<DT_PAIR> {
+  static constexpr int D = 16;
+  using Key = u64;
+  using Unit = uint4;
+  static constexpr int B = 32;      // 512 B blocks
+  static constexpr int KIDX = 256;
+  static constexpr int BASE_CAP = 12288;
+  static constexpr int CLS_THREADS = 512;
+  static constexpr int CLS_TILE = 1024;
+  static constexpr int KEY_UNITS = 1;
+  __device__ __forceinline__ static Key key(const char *e) { return *reinterpret_cast<const u64 *>(e); }
+};
+
+template <> struct Traits<DT_REC100> {
+  static constexpr int D = 100;
+  using Key = u128;                 // 80-bit big-endian key in the low 80 bits
+  using Unit = u32;
+  static constexpr int B = 8;       // 800 B blocks = 25 x 32 B sectors
+  static constexpr int KIDX = 128;
+  static constexpr int BASE_CAP = 1792;
+  static constexpr int CLS_THREADS = 256;
+  static constexpr int CLS_TILE = 256;
+  static constexpr int KEY_UNITS = 3;
+  __device__ __forceinline__ static Key key(const char *e) {
+    const u32 *w = reinterpret_cast<const u32 *>(e);
+    u64 hi = ((u64)bswap32(w[0]) << 32) | (u64)bswap32(w[1]);
+    u32 lo = bswap32(w[2]) >> 16;
+    return ((u128)hi << 16) | (u128)lo;
+  }
+};
+
+// ------------------------------------------------------------------ key helpers
+template <class K> __host__ __device__ __forceinline__ K key_from_words(const u64 *w);
+template <> __host__ __device__ __forceinline__ u64 key_from_words<u64>(const u64 *w) { return w[0]; }
+template <> __host__ __device__ __forceinline__ u128 key_from_words<u128>(const u64 *w) {
+  return ((u128)w[1] << 64) | (u128)w[0];
+}
+template <class K> __host__ __device__ __forceinline__ void key_to_words(K k, u64 *w);
+template <> __host__ __device__ __forceinline__ void key_to_words<u64>(u64 k, u64 *w) { w[0] = k; w[1] = 0; }
+template <> __host__ __device__ __forceinline__ void key_to_words<u128>(u128 k, u64 *w) {
+  w[0] = (u64)k;
+  w[1] = (u64)(k >> 64);
+}
+
+__device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
+__device__ __forceinline__ int bitlen(u128 x) {
+  u64 h = (u64)(x >> 64);
+  return h ? 128 - __clzll((long long)h) : bitlen((u64)x);
+}
+__device__ __forceinline__ u32 digit_of(u64 x, int shift, u32 mask) { return (u32)(x >> shift) & mask; }
+__device__ __forceinline__ u32 digit_of(u128 x, int shift, u32 mask) { return (u32)(x >> shift) & mask; }
+
+template <class K> __host__ __device__ __forceinline__ K key_max();
+template <> __host__ __device__ __forceinline__ u64 key_max<u64>() { return ~0ull; }
+template <> __host__ __device__ __forceinline__ u128 key_max<u128>() { return (((u128)1) << 80) - 1; }
+
+// ------------------------------------------------------------------ RNG (DESIGN R8)
+constexpr u64 GAMMA = 0x9E3779B97F4A7C15ull;
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// index of sample j of the task (begin, size) at `level`
+__device__ __forceinline__ u64 sample_index(u64 seed, u32 level, u64 begin, u64 size, u64 j) {
+  u64 base = mix64(seed + GAMMA * ((u64)level + 1)) ^ mix64(begin + GAMMA * (size + 1));
+  u64 u = mix64(base + GAMMA * (j + 1));
+  return begin + __umul64hi(u, size);
+}
+
+// ------------------------------------------------------------------ memory helpers
+__device__ __forceinline__ u64 ld_acquire_u64(const u64 *p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64 *p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  u32 s = (u32)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Copy bytes [g, g + nbytes) (g and nbytes multiples of 4) into shared memory
+// at s + (g & 15) with 16-byte cp.async for the aligned body and 4-byte
+// cp.async for the unaligned head/tail; returns the head offset (g & 15).
+// Reads never leave [g & ~15, g + nbytes) rounded to 4 B, i.e. never past the
+// end of the array.  Executed by `nthr` threads with index `tid`.
+__device__ __forceinline__ int tile_load_async(char *s, const char *g, u64 nbytes, int tid, int nthr) {
+  const uintptr_t a = (uintptr_t)g;
+  const uintptr_t a0 = a & ~(uintptr_t)15;  // smem byte s[x - a0] holds global byte x
+  const int head = (int)(a - a0);
+  const uintptr_t end = a + nbytes;
+  uintptr_t body0 = (a + 15) & ~(uintptr_t)15;
+  uintptr_t body1 = end & ~(uintptr_t)15;
+  if (body1 < body0) body1 = body0;  // tiny range: all of it is head/tail words
+  // head words [a, min(body0, end))
+  const uintptr_t hend = body0 < end ? body0 : end;
+  const int nh = (int)((hend - a) >> 2);
+  if (tid < nh) cp_async4(s + head + 4 * tid, (const void *)(a + 4 * tid));
+  // body
+  const u64 nb = (u64)((body1 - body0) >> 4);
+  const u64 boff = (u64)(body0 - a0);
+  for (u64 i = tid; i < nb; i += nthr) cp_async16(s + boff + 16 * i, (const void *)(body0 + 16 * i));
+  // tail words [max(body1, hend), end)
+  const uintptr_t t0 = body1 > hend ? body1 : hend;
+  const int nt = end > t0 ? (int)((end - t0) >> 2) : 0;
+  if (tid < nt) cp_async4(s + (t0 - a0) + 4 * tid, (const void *)(t0 + 4 * tid));
+  return head;
+}
+
+// ------------------------------------------------------------------ block scan
+// Exclusive scan of one u32 per thread over the first `n` threads of a CTA of
+// NT threads (n <= NT).  `ws` must hold NT/32 + 1 u32.  Returns the exclusive
+// prefix; *total gets the sum.  Contains __syncthreads.
+template <int NT>
+__device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *ws, u32 *total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u32 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = lane < NT / 32 ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) ws[lane] = w;  // inclusive warp totals
+    if (lane == NT / 32 - 1) ws[NT / 32] = w;
+  }
+  __syncthreads();
+  u32 pre = (wid > 0 ? ws[wid - 1] : 0) + x - v;
+  *total = ws[NT / 32];
+  __syncthreads();
+  return pre;
+}
+
+}  // namespace ips4o

@@ -1,0 +1,104 @@
+// internal.h -- data structures shared by the host driver and the kernels.
+// Product code: never includes anything from oracle/.
+#pragma once
+#include <cstdint>
+
+namespace ips4o {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef long long i64;
+typedef unsigned __int128 u128;
+
+enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3 };
+enum { ALGO_TREE = 0, ALGO_DIGIT = 1 };
+
+// Flags of a task / bucket.
+enum : u32 {
+  TF_NONE = 0,
+};
+
+// A task T[l, r): the subarray [begin, begin+size) of the input, with
+// inclusive bounds [lo, hi] on its keys in the internal order-preserving key
+// space (u64 for U64/F64/PAIR, 80-bit for REC100; stored as two u64 words).
+struct TaskDesc {
+  u64 begin;
+  u64 size;
+  u64 lo[2];  // [0] = low 64 bits, [1] = high bits
+  u64 hi[2];
+  u32 level;
+  u32 flags;
+};
+
+// Per-task record of one partitioning level.  The host fills the plan part;
+// the kernels fill the result part.
+struct LevelTask {
+  TaskDesc t;
+  // ---- plan (host)
+  u32 k_req;         // requested leaves (TREE) / max digits (DIGIT), power of 2
+  u32 kidx;          // capacity of this task's per-bucket arrays (>= K)
+  u32 m;             // samples to draw (TREE), m = alpha * k_req
+  u32 stripe_first;  // first stripe of this task in the level's stripe list
+  u32 nstripes;
+  u32 perm_first;    // first permute CTA
+  u32 nperm;         // permute CTAs
+  u32 pad0;
+  u64 stripe_elems;  // elements per stripe (multiple of b); last stripe shorter
+  u64 bucket_off;    // offset (in bucket slots) into per-task-bucket arrays
+  u64 sbk_off;       // offset (in stripe-bucket slots) of this task's first stripe;
+                     // stripe s uses slots [sbk_off + (s - stripe_first) * kidx, +kidx)
+  // ---- results (device)
+  u32 K;             // number of bucket indices of the classifier
+  u32 l;             // log2(leaves) (TREE) or digit bits (DIGIT)
+  u32 equality;      // equality buckets on (TREE)
+  int shift;         // digit shift (DIGIT)
+  u32 k_used;        // k after the equality-budget rule (DESIGN R10)
+  u32 pad1;
+};
+
+// Device pointers of one level's scratch arrays (all in one arena).
+struct LevelArgs {
+  char *base;                 // the input array
+  LevelTask *tasks;           // [ntasks]
+  u32 ntasks;
+  u32 nstripes;
+  u32 nperm;                  // permute CTAs in total
+  u32 algo;
+  const u32 *stripe_task;     // [nstripes] -> task index
+  const u32 *perm_task;       // [nperm] -> task index
+  void *trees;                // [ntasks][2][KIDX] keys (tree | splitter)
+  u32 *counts;                // [stripe-bucket slot] elements per bucket per stripe
+  u32 *pfill;                 // [stripe-bucket slot] elements left in partial buffers
+  u32 *fullblocks;            // [nstripes] full blocks flushed per stripe
+  char *partials;             // [stripe-bucket slot][b*D] partial buffer contents
+  u64 *E;                     // [bucket_off + j], j <= K: exact boundaries (relative)
+  u32 *fblk;                  // [bucket_off + j]: full blocks of bucket j (task-wide)
+  u64 *wr;                    // [bucket_off + j] * 8 words: packed (w, r) at [0], readers at [4]
+  char *overlap;              // [bucket_off + j][b*D] saved overlaps (cleanup phase a)
+  char *overflow;             // [ntasks][b*D] overflow blocks
+  u32 *ovf_used;              // [ntasks] bucket that wrote the overflow block, or ~0
+  // scheduler outputs
+  TaskDesc *next_tasks;       // next level
+  TaskDesc *base_tasks;       // base-case tasks of this level
+  u32 *counters;              // [0] next count, [1] base count, [2] equal elems lo, [3] hi
+  u32 next_cap;
+  u32 base_cap_tasks;
+  u64 base_cap_elems;         // base-case capacity M (elements)
+  u64 seed;
+};
+
+// The packed per-bucket permutation word: high 32
+// bits = write pointer w (block index), low 32 bits = read pointer r + RBIAS
+// (r is the inclusive index of the last unprocessed block; it may fall below
+// w by at most the number of agents, hence the bias).
+constexpr u64 RBIAS = 1ull << 31;
+constexpr int WR_STRIDE = 8;      // u64 words per bucket slot (64 B): [0]=wr, [4]=readers
+
+struct PrepassOut {
+  u32 nondecreasing;  // all adjacent pairs a[i] <= a[i+1]
+  u32 nonincreasing;  // all adjacent pairs a[i] >= a[i+1]
+  u64 minkey[2];
+  u64 maxkey[2];
+};
+
+}  // namespace ips4o

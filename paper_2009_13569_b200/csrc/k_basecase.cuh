@@ -1,0 +1,227 @@
+// k_basecase.cuh -- K7: the base case, "small buckets are finished inside one
+// CTA in shared memory" (north star; P:980-982 and P:1652 use insertion sort
+// on CPUs).  One CTA per bucket of at most M elements:
+//   1. histogram of a digit of (key - lo) over the bucket's key bounds [lo,hi]
+//      (the bounds come from the splitters, so the digit splits the bucket
+//      into ~m/8 nearly equal runs),
+//   2. exclusive scan, scatter into shared memory (second, L2-resident read),
+//   3. sort every run: insertion sort for short runs (the paper's base case,
+//      P:1652), a warp bitonic network in shared memory for longer ones,
+//   4. coalesced write-back.
+#pragma once
+#include "common.cuh"
+
+namespace ips4o {
+
+template <int DT> struct BaseItem;
+
+template <> struct BaseItem<DT_U64> {
+  using Item = u64;
+  using Key = u64;
+  static constexpr int THREADS = 1024, DBMAX = 11, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = false;
+  __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
+  __device__ static Key key(const Item &it) { return it; }
+  __device__ static bool less(const Item &a, const Item &b) { return a < b; }
+};
+template <> struct BaseItem<DT_F64> {
+  using Item = u64;  // order-preserving key
+  using Key = u64;
+  static constexpr int THREADS = 1024, DBMAX = 11, CAP = Traits<DT_F64>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = false;
+  __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
+  __device__ static Key key(const Item &it) { return it; }
+  __device__ static bool less(const Item &a, const Item &b) { return a < b; }
+};
+struct alignas(16) PairItem {
+  u64 key, val;
+};
+template <> struct BaseItem<DT_PAIR> {
+  using Item = PairItem;
+  using Key = u64;
+  static constexpr int THREADS = 512, DBMAX = 11, CAP = Traits<DT_PAIR>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = false;
+  __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const PairItem *>(e); }
+  __device__ static Key key(const Item &it) { return it.key; }
+  __device__ static bool less(const Item &a, const Item &b) { return a.key < b.key; }
+};
+template <> struct BaseItem<DT_REC100> {
+  using Item = u128;  // key80 << 16 | index of the record in the staging area
+  using Key = u128;
+  static constexpr int THREADS = 512, DBMAX = 9, CAP = Traits<DT_REC100>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = true;
+  __device__ static Item load(const char *e, u32 idx) { return (Traits<DT_REC100>::key(e) << 16) | (u128)idx; }
+  __device__ static Key key(const Item &it) { return it >> 16; }
+  __device__ static bool less(const Item &a, const Item &b) { return a < b; }
+};
+
+template <int DT> struct BaseSmem {
+  using BI = BaseItem<DT>;
+  static constexpr size_t off_items = 0;
+  static constexpr size_t off_rec = off_items + (size_t)BI::CAP * sizeof(typename BI::Item);
+  static constexpr size_t off_hist =
+      off_rec + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * Traits<DT>::D + 15) / 16 * 16 : 0);
+  static constexpr size_t off_big = off_hist + ((size_t)1 << BI::DBMAX) * 4;
+  static constexpr int BIGCAP = 1 << BI::DBMAX;
+  static constexpr size_t bytes = off_big + (size_t)BIGCAP * 4 + (BI::THREADS / 32 + 4) * 4;
+};
+
+template <class BI>
+__device__ __forceinline__ void insertion_sort_run(typename BI::Item *a, int n) {
+  for (int i = 1; i < n; ++i) {
+    typename BI::Item x = a[i];
+    int j = i;
+    while (j > 0 && BI::less(x, a[j - 1])) {
+      a[j] = a[j - 1];
+      --j;
+    }
+    a[j] = x;
+  }
+}
+
+// Warp bitonic sort of a[0..n) in shared memory.  All comparators point the
+// same way (the "flip" form), so the virtual +inf padding to the next power of
+// two never moves and comparators that touch it are skipped.
+template <class BI>
+__device__ void warp_bitonic_run(typename BI::Item *a, int n, int lane) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int q = lane; q < P / 2; q += 32) {
+        int i, p;
+        if (j == (k >> 1)) {  // flip step
+          int blk = q / j, off = q % j;
+          i = blk * k + off;
+          p = blk * k + (k - 1 - off);
+        } else {
+          int blk = q / j, off = q % j;
+          i = blk * 2 * j + off;
+          p = i + j;
+        }
+        if (p < n) {
+          typename BI::Item x = a[i], y = a[p];
+          if (BI::less(y, x)) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
+    basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap) {
+  using Tr = Traits<DT>;
+  using BI = BaseItem<DT>;
+  using Item = typename BI::Item;
+  using Key = typename BI::Key;
+  using S = BaseSmem<DT>;
+  constexpr int NT = BI::THREADS, D = Tr::D;
+  extern __shared__ __align__(16) char smem[];
+  Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
+  char *s_rec = smem + S::off_rec;
+  u32 *s_hist = reinterpret_cast<u32 *>(smem + S::off_hist);
+  u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
+  u32 *s_ws = s_big + S::BIGCAP;  // scan workspace (NT/32+1) + nbig
+  __shared__ u32 s_nbig;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  u32 count = *count_ptr;
+  if (count > count_cap) count = count_cap;
+
+  for (u32 ti = blockIdx.x; ti < count; ti += gridDim.x) {
+    const TaskDesc t = tasks[ti];
+    const int m = (int)t.size;
+    char *g = base + t.begin * (u64)D;
+    const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
+    if (m <= 1 || !(lo < hi)) continue;
+    const int bits = bitlen((Key)(hi - lo));
+    int db = 1;
+    while ((1 << (db + 3)) < m && db < BI::DBMAX) ++db;  // ~8 elements per digit
+    if (db > bits) db = bits;
+    const int shift = bits - db;
+    const int nd = (int)((hi - lo) >> shift) + 1;  // digits in use, <= 2^db
+
+    for (int d = tid; d < nd; d += NT) s_hist[d] = 0;
+    if (tid == 0) s_nbig = 0;
+    if constexpr (BI::STAGE_RECORDS) {
+      // stage the records (coalesced u32 copy)
+      const u32 *src = reinterpret_cast<const u32 *>(g);
+      u32 *dst = reinterpret_cast<u32 *>(s_rec);
+      for (int w = tid; w < m * (D / 4); w += NT) dst[w] = src[w];
+    }
+    __syncthreads();
+    // 1. histogram
+    for (int i = tid; i < m; i += NT) {
+      const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
+      Item it = BI::load(e, (u32)i);
+      u32 d = (u32)((BI::key(it) - lo) >> shift);
+      atomicAdd(&s_hist[d], 1u);
+    }
+    __syncthreads();
+    // 2. exclusive scan in place (chunked)
+    u32 carry = 0;
+    for (int b0 = 0; b0 < nd; b0 += NT) {
+      int d = b0 + tid;
+      u32 v = d < nd ? s_hist[d] : 0;
+      u32 tot;
+      u32 p = block_exclusive_scan<NT>(v, s_ws, &tot);
+      if (d < nd) s_hist[d] = carry + p;
+      carry += tot;
+    }
+    __syncthreads();
+    // scatter (s_hist[d] becomes the END of run d)
+    for (int i = tid; i < m; i += NT) {
+      const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
+      Item it = BI::load(e, (u32)i);
+      u32 d = (u32)((BI::key(it) - lo) >> shift);
+      u32 pos = atomicAdd(&s_hist[d], 1u);
+      s_items[pos] = it;
+    }
+    __syncthreads();
+    // 3. sort the runs [end[d-1], end[d])
+    for (int d = tid; d < nd; d += NT) {
+      int a = d ? (int)s_hist[d - 1] : 0;
+      int n = (int)s_hist[d] - a;
+      if (n <= 1) continue;
+      if (shift == 0) continue;  // all keys of the run are equal
+      if (n <= 16) {
+        insertion_sort_run<BI>(s_items + a, n);
+      } else {
+        u32 slot = atomicAdd(&s_nbig, 1u);
+        s_big[slot] = (u32)d;
+      }
+    }
+    __syncthreads();
+    const int nbig = (int)s_nbig;
+    for (int q = wid; q < nbig; q += NT / 32) {
+      int d = (int)s_big[q];
+      int a = d ? (int)s_hist[d - 1] : 0;
+      int n = (int)s_hist[d] - a;
+      warp_bitonic_run<BI>(s_items + a, n, lane);
+    }
+    __syncthreads();
+    // 4. write back
+    if constexpr (DT == DT_U64 || DT == DT_PAIR) {
+      Item *out = reinterpret_cast<Item *>(g);
+      for (int i = tid; i < m; i += NT) out[i] = s_items[i];
+    } else if constexpr (DT == DT_F64) {
+      u64 *out = reinterpret_cast<u64 *>(g);
+      for (int i = tid; i < m; i += NT) out[i] = key_to_f64((u64)BI::key(s_items[i]));
+    } else {
+      // records: warp per record, lanes copy the 25 words
+      u32 *out = reinterpret_cast<u32 *>(g);
+      for (int i = wid; i < m; i += NT / 32) {
+        const u32 idx = (u32)(s_items[i] & (Item)0xFFFF);
+        const u32 *src = reinterpret_cast<const u32 *>(s_rec + (size_t)idx * D);
+        if (lane < D / 4) out[(size_t)i * (D / 4) + lane] = src[lane];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace ips4o

@@ -1,0 +1,261 @@
+// k_classify.cuh -- K2: classification with block buffers (P:739-780,
+// Figs. 4/5 P:745-760).  One CTA per stripe.  The CTA streams its stripe
+// through shared-memory tiles (cp.async double buffering), classifies each
+// element with the branchless tree (Alg. 1, batched per thread like
+// the paper's unrolled loop) or the IPS2Ra digit, appends it to one of K
+// shared-memory buffer blocks of b elements, and writes every full block back
+// to the front of its own stripe (there is always room because at
+// least b more elements were read than written).  Per-bucket counts come for
+// free.  At the end the partially filled buffers are spilled to
+// scratch (they are the "partial buffers" of the cleanup).
+//
+// Tile-synchronous form (SURVEY 7/H2 option B): per tile, bucket ranks come
+// from shared-memory atomics, a CTA-wide scan over the K buckets yields the
+// blocks each bucket emits, and warps write whole blocks with coalesced
+// stores.  Elements of an emitted block come from the bucket's buffer (older
+// elements) followed by tile elements (gathered through an index list).
+#pragma once
+#include "common.cuh"
+
+namespace ips4o {
+
+template <class Key>
+__device__ __forceinline__ u32 tree_bucket(const Key *tree, const Key *spl, int l, int eq, Key e) {
+  u32 i = 1;
+  for (int r = 0; r < l; ++r) i = 2 * i + (tree[i] < e ? 1u : 0u);
+  u32 leaf = i - (1u << l);
+  if (!eq) return leaf;
+  return 2 * leaf + 1 - (e < spl[leaf] ? 1u : 0u);
+}
+
+// Alg. 1: one tree level across all IPT elements before the next level.
+template <class Key, int IPT>
+__device__ __forceinline__ void tree_bucket_batch(const Key *tree, const Key *spl, int l, int eq,
+                                                  const Key (&e)[IPT], u32 (&b)[IPT]) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) b[k] = 1;
+  for (int r = 0; r < l; ++r) {
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) b[k] = 2 * b[k] + (tree[b[k]] < e[k] ? 1u : 0u);
+  }
+  const u32 half = 1u << l;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    u32 leaf = b[k] - half;
+    b[k] = eq ? 2 * leaf + 1 - (e[k] < spl[leaf] ? 1u : 0u) : leaf;
+  }
+}
+
+template <int DT>
+struct ClsSmem {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  static constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX, T = Tr::CLS_TILE, NT = Tr::CLS_THREADS;
+  static constexpr int TILE_BYTES = ((T * D + 16) + 15) / 16 * 16;
+  static constexpr size_t off_buf = 0;
+  static constexpr size_t off_tiles = off_buf + (size_t)KI * B * D;
+  static constexpr size_t off_tree = (off_tiles + 2 * TILE_BYTES + 15) / 16 * 16;
+  static constexpr size_t off_u32 = off_tree + 2 * KI * sizeof(Key);
+  // u32 arrays: fill, tcnt, cnt, boff, eoff, nb  (KI each) + ws (NT/32 + 1)
+  static constexpr size_t off_idx = off_u32 + (6 * KI + NT / 32 + 1) * 4;
+  static constexpr size_t bytes = (off_idx + T * 2 + 15) / 16 * 16;
+};
+
+template <int DT, int ALGO>
+__global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  using Unit = typename Tr::Unit;
+  using S = ClsSmem<DT>;
+  constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX, T = Tr::CLS_TILE, NT = Tr::CLS_THREADS;
+  constexpr int IPT = T / NT;
+  constexpr int UPE = D / (int)sizeof(Unit);  // units per element
+  constexpr int NWARPS = NT / 32;
+  static_assert(T % NT == 0, "tile must be a multiple of the CTA size");
+  static_assert(KI <= NT, "one thread per bucket in the scans");
+  static_assert(T < 65536 && T / B + KI < 65536, "16-bit scan packing");
+
+  extern __shared__ __align__(16) char smem[];
+  char *s_buf = smem + S::off_buf;
+  char *s_tiles = smem + S::off_tiles;
+  Key *s_tree = reinterpret_cast<Key *>(smem + S::off_tree);
+  Key *s_spl = s_tree + KI;
+  u32 *s_fill = reinterpret_cast<u32 *>(smem + S::off_u32);
+  u32 *s_tcnt = s_fill + KI;
+  u32 *s_cnt = s_tcnt + KI;
+  u32 *s_boff = s_cnt + KI;
+  u32 *s_eoff = s_boff + KI;
+  u32 *s_nb = s_eoff + KI;
+  u32 *s_ws = s_nb + KI;
+  unsigned short *s_idx = reinterpret_cast<unsigned short *>(smem + S::off_idx);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 stripe = blockIdx.x;
+  const u32 ti = A.stripe_task[stripe];
+  const LevelTask &L = A.tasks[ti];
+  const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
+  const u32 dmask = L.K - 1;
+  const u64 size = L.t.size;
+  const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
+  const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
+  char *gtask = A.base + L.t.begin * (u64)D;
+
+  if (ALGO == ALGO_TREE) {
+    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
+    const int leaves = 1 << l;
+    for (int i = tid; i < leaves; i += NT) {
+      s_tree[i] = gt[i];
+      s_spl[i] = gt[KI + i];
+    }
+  }
+  for (int j = tid; j < KI; j += NT) {
+    s_fill[j] = 0;
+    s_tcnt[j] = 0;
+    s_cnt[j] = 0;
+  }
+
+  const u64 n = s1 > s0 ? s1 - s0 : 0;
+  const u64 ntiles = (n + T - 1) / T;
+  u64 front = 0;  // blocks flushed so far (relative to the stripe start)
+
+  if (ntiles > 0) {
+    u64 c0 = n < (u64)T ? n : (u64)T;
+    tile_load_async(s_tiles, gtask + s0 * D, c0 * D, tid, NT);
+  }
+  cp_async_commit();
+
+  for (u64 t = 0; t < ntiles; ++t) {
+    const int stage = (int)(t & 1);
+    const u64 e0 = s0 + t * T;  // first element of this tile (task-relative)
+    const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
+    if (t + 1 < ntiles) {
+      const u64 e1 = e0 + T;
+      const u64 c1 = (s1 - e1) < (u64)T ? (s1 - e1) : (u64)T;
+      tile_load_async(s_tiles + (1 - stage) * S::TILE_BYTES, gtask + e1 * D, c1 * D, tid, NT);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const char *tp = s_tiles + stage * S::TILE_BYTES + (int)(((uintptr_t)(gtask + e0 * D)) & 15);
+
+    // ---- classify (Alg. 1 batched over IPT elements per thread)
+    Key key[IPT];
+    u32 bkt[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int i = tid + k * NT;
+      key[k] = i < cnt ? Tr::key(tp + (size_t)i * D) : (Key)0;
+    }
+    if (ALGO == ALGO_TREE) {
+      tree_bucket_batch<Key, IPT>(s_tree, s_spl, l, eq, key, bkt);
+    } else {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+    }
+    u32 rank[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int i = tid + k * NT;
+      rank[k] = i < cnt ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;
+    }
+    __syncthreads();
+
+    // ---- per-bucket plan: blocks to emit (nb) and tile elements they take (em)
+    u32 tc = 0, tot = 0, nb = 0, em = 0;
+    if (tid < KI) {
+      tc = s_tcnt[tid];
+      tot = s_fill[tid] + tc;
+      nb = tot / B;
+      em = nb ? nb * B - s_fill[tid] : 0;
+    }
+    u32 total;
+    u32 pre = block_exclusive_scan<NT>((nb << 16) | em, s_ws, &total);
+    if (tid < KI) {
+      s_boff[tid] = pre >> 16;
+      s_eoff[tid] = pre & 0xFFFFu;
+      s_nb[tid] = nb;
+      s_cnt[tid] += tc;
+    }
+    const u32 nblocks = total >> 16;
+    __syncthreads();
+
+    // ---- stage the tile elements of emitted blocks (index list)
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int i = tid + k * NT;
+      if (i < cnt) {
+        u32 j = bkt[k];
+        u32 v = s_fill[j] + rank[k];
+        if (v < s_nb[j] * B) s_idx[s_eoff[j] + rank[k]] = (unsigned short)i;
+      }
+    }
+    __syncthreads();
+
+    // ---- emit full blocks to the stripe's write front (coalesced per warp)
+    for (u32 g = wid; g < nblocks; g += NWARPS) {
+      // bucket j = last index with boff[j] <= g (it has nb > 0)
+      int lo = 0, hi = KI;  // find first index with boff > g
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (s_boff[mid] <= g) lo = mid + 1;
+        else hi = mid;
+      }
+      const int j = lo - 1;
+      const u32 q = g - s_boff[j];
+      const u32 bf = s_fill[j];
+      const u32 eo = s_eoff[j];
+      Unit *dst = reinterpret_cast<Unit *>(gtask + (s0 + (front + s_boff[j] + q) * B) * D);
+      for (int u = lane; u < B * UPE; u += 32) {
+        const int e = u / UPE, w = u - e * UPE;
+        const u32 v = q * B + e;
+        const char *src = v < bf ? s_buf + ((size_t)j * B + v) * D
+                                 : tp + (size_t)s_idx[eo + v - bf] * D;
+        dst[u] = reinterpret_cast<const Unit *>(src)[w];
+      }
+    }
+    front += nblocks;
+    __syncthreads();
+
+    // ---- remaining tile elements go to the (now free) buffer slots
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int i = tid + k * NT;
+      if (i < cnt) {
+        u32 j = bkt[k];
+        u32 v = s_fill[j] + rank[k];
+        u32 cut = s_nb[j] * B;
+        if (v >= cut) {
+          const Unit *src = reinterpret_cast<const Unit *>(tp + (size_t)i * D);
+          Unit *dst = reinterpret_cast<Unit *>(s_buf + ((size_t)j * B + (v - cut)) * D);
+#pragma unroll
+          for (int w = 0; w < UPE; ++w) dst[w] = src[w];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < KI) {
+      s_fill[tid] = tot - nb * B;
+      s_tcnt[tid] = 0;
+    }
+    // the next iteration's __syncthreads orders these updates
+  }
+  __syncthreads();
+
+  // ---- outputs: counts, partial fill, full blocks, partial buffers
+  const u64 sbase = L.sbk_off + (u64)(stripe - L.stripe_first) * L.kidx;
+  for (int j = tid; j < (int)L.kidx; j += NT) {
+    A.counts[sbase + j] = s_cnt[j];
+    A.pfill[sbase + j] = s_fill[j];
+  }
+  if (tid == 0) A.fullblocks[stripe] = (u32)front;
+  for (int j = wid; j < K; j += NWARPS) {
+    const int f = (int)s_fill[j];
+    const Unit *src = reinterpret_cast<const Unit *>(s_buf + (size_t)j * B * D);
+    Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * D);
+    for (int u = lane; u < f * UPE; u += 32) dst[u] = src[u];
+  }
+}
+
+}  // namespace ips4o

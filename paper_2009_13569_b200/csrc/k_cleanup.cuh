@@ -1,0 +1,209 @@
+// k_cleanup.cuh -- K5 cleanup and K6 the recursion scheduler
+// (Alg. 2, adapted to device task lists).
+#pragma once
+#include "common.cuh"
+#include "k_classify.cuh"
+
+namespace ips4o {
+
+// ------------------------------------------------------------------ K5a
+// Phase a (one warp per bucket): save the elements of bucket j that its last
+// block wrote past E_{j+1} into bucket j+1's head ("the head of
+// b_{i+1}") -- logical positions [E_{j+1}, w_j*b) -- and, for the bucket that
+// used the overflow block, copy the in-array part of that block to its
+// final place [p*b, E_{j+1}).  Phase b then only writes holes.
+constexpr int CLN_WARPS = 8;
+
+template <int DT>
+__global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Unit = typename Tr::Unit;
+  constexpr int D = Tr::D, B = Tr::B;
+  constexpr int UPE = D / (int)sizeof(Unit);
+  const u32 ti = blockIdx.y;
+  const LevelTask &L = A.tasks[ti];
+  const int j = blockIdx.x * CLN_WARPS + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= (int)L.K) return;
+  const u64 bo = L.bucket_off;
+  const u64 size = L.t.size;
+  const u64 pblk = (size % B) ? size / B : ~0ull;
+  const u32 ovb = A.ovf_used[ti];
+  const char *ovf = A.overflow + (size_t)ti * B * D;
+  char *gtask = A.base + L.t.begin * (u64)D;
+  const u64 W = (A.wr[(bo + j) * WR_STRIDE] >> 32) * (u64)B;  // logical end of bucket j's blocks
+  const u64 E1 = A.E[bo + j + 1];
+  auto logical = [&](u64 x) -> const Unit * {
+    if (ovb == (u32)j && x >= pblk * B) return reinterpret_cast<const Unit *>(ovf + (x - pblk * B) * D);
+    return reinterpret_cast<const Unit *>(gtask + x * D);
+  };
+  if (W > E1) {
+    const u64 o = W - E1;  // < b
+    Unit *dst = reinterpret_cast<Unit *>(A.overlap + (bo + j) * (u64)B * D);
+    for (u64 u = lane; u < o * UPE; u += 32) {
+      u64 e = u / UPE, w = u % UPE;
+      dst[u] = logical(E1 + e)[w];
+    }
+  }
+  if (ovb == (u32)j) {
+    const u64 p0 = pblk * B;
+    const u64 hi = E1 < size ? E1 : size;
+    for (u64 u = lane; p0 + u / UPE < hi; u += 32) {
+      u64 e = u / UPE, w = u % UPE;
+      reinterpret_cast<Unit *>(gtask + (p0 + e) * D)[w] = reinterpret_cast<const Unit *>(ovf + e * D)[w];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5b
+// Phase b (one CTA per bucket): fill the holes of bucket j -- its head
+// [E_j, min(d_j, E_{j+1})) and its tail [w_j*b, E_{j+1}) -- with the saved
+// overlap of bucket j and the partial buffers of every stripe of the task
+// (the misplaced elements are in the head of b_{i+1}, in the
+// partially filled buffers, or in the overflow block).
+constexpr int FILL_THREADS = 256;
+
+template <int DT>
+__global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Unit = typename Tr::Unit;
+  constexpr int D = Tr::D, B = Tr::B;
+  constexpr int UPE = D / (int)sizeof(Unit);
+  extern __shared__ __align__(16) u32 s_cum[];  // [nstripes + 1]
+  __shared__ u32 ws[FILL_THREADS / 32 + 1];
+  const u32 ti = blockIdx.y;
+  const LevelTask &L = A.tasks[ti];
+  const int j = blockIdx.x;
+  if (j >= (int)L.K) return;
+  const u64 bo = L.bucket_off;
+  const u64 E0 = A.E[bo + j], E1 = A.E[bo + j + 1];
+  if (E1 == E0) return;
+  const u64 d0 = (E0 + B - 1) / B * B;
+  const u64 W = (A.wr[(bo + j) * WR_STRIDE] >> 32) * (u64)B;
+  const u64 hd = d0 < E1 ? d0 : E1;     // head hole [E0, hd)
+  const u64 tl = W > hd ? W : hd;       // tail hole [tl, E1) if tl < E1
+  const u64 nhead = hd - E0;
+  const u64 ntail = tl < E1 ? E1 - tl : 0;
+  const u64 nholes = nhead + ntail;
+  const u64 o = W > E1 ? W - E1 : 0;    // saved overlap elements
+  const u32 nst = L.nstripes;
+  u32 carry = 0;
+  for (u32 base = 0; base < nst; base += FILL_THREADS) {
+    u32 idx = base + threadIdx.x;
+    u32 v = idx < nst ? A.pfill[L.sbk_off + (u64)idx * L.kidx + j] : 0;
+    u32 tot;
+    u32 p = block_exclusive_scan<FILL_THREADS>(v, ws, &tot);
+    if (idx < nst) s_cum[idx] = carry + p;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    s_cum[nst] = carry;
+    // invariant of the cleanup: #holes = overlap + partial buffers (+ overflow,
+    // already moved in phase a); a violation is reported, never silent
+    if (nholes != o + carry) atomicAdd(&A.counters[4], 1u);
+  }
+  __syncthreads();
+  if (nholes == 0) return;
+  char *gtask = A.base + L.t.begin * (u64)D;
+  const char *ovl = A.overlap + (bo + j) * (u64)B * D;
+  for (u64 h = threadIdx.x; h < nholes; h += FILL_THREADS) {
+    const u64 pos = h < nhead ? E0 + h : tl + (h - nhead);
+    const char *src;
+    if (h < o) {
+      src = ovl + h * D;
+    } else {
+      const u32 g = (u32)(h - o);
+      int lo = 0, hi = (int)nst;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (s_cum[mid] <= g) lo = mid + 1;
+        else hi = mid;
+      }
+      const int s = lo - 1;
+      src = A.partials + ((L.sbk_off + (u64)s * L.kidx + j) * B + (g - s_cum[s])) * D;
+    }
+    const Unit *su = reinterpret_cast<const Unit *>(src);
+    Unit *du = reinterpret_cast<Unit *>(gtask + pos * D);
+#pragma unroll
+    for (int w = 0; w < UPE; ++w) du[w] = su[w];
+  }
+}
+
+// ------------------------------------------------------------------ K6
+// Scheduler: turn the buckets of every task into child tasks.
+// Equality buckets (odd index 2i+1, i < s) are terminal; buckets
+// of at most one element are done; buckets of at most M elements (the
+// one-CTA base-case capacity, the GPU analogue of "at most 2 n_0")
+// go to the base-case list; the rest form the next level.  Child key bounds
+// come from the splitters (TREE) or the digit (DIGIT).
+constexpr int SCHED_THREADS = 256;
+
+template <int DT, int ALGO>
+__global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  constexpr int KI = Tr::KIDX;
+  const u32 ti = blockIdx.x;
+  const LevelTask &L = A.tasks[ti];
+  const int K = (int)L.K;
+  const Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
+  const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
+  const Key *spl = gt + KI;
+  for (int j = threadIdx.x; j < K; j += SCHED_THREADS) {
+    const u64 e0 = A.E[L.bucket_off + j], e1 = A.E[L.bucket_off + j + 1];
+    const u64 sz = e1 - e0;
+    if (sz == 0) continue;
+    Key lo = plo, hi = phi;
+    bool terminal = false;
+    if (ALGO == ALGO_TREE) {
+      const int s = (1 << L.l) - 1;
+      if (L.equality) {
+        const int i = j >> 1;
+        if ((j & 1) && i < s) {
+          lo = hi = spl[i];
+          terminal = true;
+        } else {
+          // keys in (s_{i-1}, s_i) for i < s, or (s_{s-1}, +inf) for i = s
+          if (i > 0) lo = spl[i - 1] + 1;
+          if (i < s) hi = spl[i] - 1;
+        }
+      } else {
+        // keys in (s_{j-1}, s_j]
+        if (j > 0) lo = spl[j - 1] + 1;
+        if (j < s) hi = spl[j];
+      }
+    } else {
+      const int bits = (int)L.l;
+      const int sb = L.shift + bits;
+      const Key top = sb >= (int)(8 * sizeof(Key)) ? (Key)0 : (plo >> sb) << sb;
+      const Key dlo = top | ((Key)(u32)j << L.shift);
+      const Key dhi = dlo | ((((Key)1) << L.shift) - 1);
+      lo = dlo;
+      hi = dhi;
+      terminal = (L.shift == 0);  // a single key value per digit
+    }
+    if (lo < plo) lo = plo;
+    if (hi > phi) hi = phi;
+    if (lo >= hi) terminal = true;  // one distinct key (or an empty range)
+    if (terminal || sz <= 1) {
+      if (sz > 1) atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[2]), (unsigned long long)sz);
+      continue;
+    }
+    TaskDesc c;
+    c.begin = L.t.begin + e0;
+    c.size = sz;
+    key_to_words<Key>(lo, c.lo);
+    key_to_words<Key>(hi, c.hi);
+    c.level = L.t.level + 1;
+    c.flags = 0;
+    if (sz <= A.base_cap_elems) {
+      u32 slot = atomicAdd(&A.counters[1], 1u);
+      if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;
+    } else {
+      u32 slot = atomicAdd(&A.counters[0], 1u);
+      if (slot < A.next_cap) A.next_tasks[slot] = c;
+    }
+  }
+}
+
+}  // namespace ips4o

@@ -1,0 +1,161 @@
+// k_misc.cuh -- K0 easy-input pre-pass (P:1654-1656 sorted-input detection;
+// IPS2Ra's significant-bit scan P:2344-2346 as min/max of the keys), K8 the
+// in-place reversal of a decreasingly sorted input, and the classifier test
+// kernel behind ips4o_classify().
+#pragma once
+#include "common.cuh"
+#include "k_classify.cuh"
+
+namespace ips4o {
+
+constexpr int PRE_THREADS = 512;
+constexpr int PRE_UNROLL = 4;
+
+struct PrepassPart {
+  u32 nd, ni, pad0, pad1;
+  u64 mn[2], mx[2];
+};
+
+template <class Key>
+__device__ __forceinline__ Key shfl_key(Key v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+template <>
+__device__ __forceinline__ u128 shfl_key<u128>(u128 v, int src) {
+  u64 lo = __shfl_sync(0xffffffffu, (u64)v, src);
+  u64 hi = __shfl_sync(0xffffffffu, (u64)(v >> 64), src);
+  return ((u128)hi << 64) | lo;
+}
+template <class Key>
+__device__ __forceinline__ Key shfl_xor_key(Key v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+template <>
+__device__ __forceinline__ u128 shfl_xor_key<u128>(u128 v, int m) {
+  u64 lo = __shfl_xor_sync(0xffffffffu, (u64)v, m);
+  u64 hi = __shfl_xor_sync(0xffffffffu, (u64)(v >> 64), m);
+  return ((u128)hi << 64) | lo;
+}
+
+// Each thread checks the adjacent pairs (i, i+1) of a grid-strided index set.
+template <int DT>
+__global__ void __launch_bounds__(PRE_THREADS) prepass_kernel(const char *base, u64 n, PrepassPart *parts) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  constexpr int D = Tr::D;
+  u32 nd = 1, ni = 1;
+  Key mn = key_max<Key>(), mx = (Key)0;
+  const u64 stride = (u64)gridDim.x * PRE_THREADS;
+  for (u64 i0 = (u64)blockIdx.x * PRE_THREADS + threadIdx.x; i0 < n; i0 += stride * PRE_UNROLL) {
+    Key a[PRE_UNROLL], b[PRE_UNROLL];
+#pragma unroll
+    for (int u = 0; u < PRE_UNROLL; ++u) {
+      u64 i = i0 + (u64)u * stride;
+      if (i < n) {
+        a[u] = Tr::key(base + i * D);
+        b[u] = (i + 1 < n) ? Tr::key(base + (i + 1) * D) : a[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PRE_UNROLL; ++u) {
+      u64 i = i0 + (u64)u * stride;
+      if (i < n) {
+        nd &= (a[u] <= b[u]) ? 1u : 0u;
+        ni &= (a[u] >= b[u]) ? 1u : 0u;
+        mn = a[u] < mn ? a[u] : mn;
+        mx = a[u] > mx ? a[u] : mx;
+      }
+    }
+  }
+  nd = __all_sync(0xffffffffu, nd);
+  ni = __all_sync(0xffffffffu, ni);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Key x = shfl_xor_key(mn, o), y = shfl_xor_key(mx, o);
+    mn = x < mn ? x : mn;
+    mx = y > mx ? y : mx;
+  }
+  __shared__ u32 s_nd[PRE_THREADS / 32], s_ni[PRE_THREADS / 32];
+  __shared__ Key s_mn[PRE_THREADS / 32], s_mx[PRE_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_nd[wid] = nd;
+    s_ni[wid] = ni;
+    s_mn[wid] = mn;
+    s_mx[wid] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < PRE_THREADS / 32; ++w) {
+      nd &= s_nd[w];
+      ni &= s_ni[w];
+      mn = s_mn[w] < mn ? s_mn[w] : mn;
+      mx = s_mx[w] > mx ? s_mx[w] : mx;
+    }
+    PrepassPart p;
+    p.nd = nd;
+    p.ni = ni;
+    p.pad0 = p.pad1 = 0;
+    key_to_words<Key>(mn, p.mn);
+    key_to_words<Key>(mx, p.mx);
+    parts[blockIdx.x] = p;
+  }
+}
+
+template <int DT>
+__global__ void prepass_reduce_kernel(const PrepassPart *parts, int nparts, PrepassOut *out) {
+  using Key = typename Traits<DT>::Key;
+  if (threadIdx.x != 0) return;
+  u32 nd = 1, ni = 1;
+  Key mn = key_max<Key>(), mx = (Key)0;
+  for (int i = 0; i < nparts; ++i) {
+    nd &= parts[i].nd;
+    ni &= parts[i].ni;
+    Key a = key_from_words<Key>(parts[i].mn), b = key_from_words<Key>(parts[i].mx);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  out->nondecreasing = nd;
+  out->nonincreasing = ni;
+  key_to_words<Key>(mn, out->minkey);
+  key_to_words<Key>(mx, out->maxkey);
+}
+
+// In-place reversal of n elements of D bytes ("reverses the input in
+// the case that the input was sorted in decreasing order").
+template <int DT>
+__global__ void reverse_kernel(char *base, u64 n) {
+  using Tr = Traits<DT>;
+  using Unit = typename Tr::Unit;
+  constexpr int UPE = Tr::D / (int)sizeof(Unit);
+  const u64 half = n / 2;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < half; i += (u64)gridDim.x * blockDim.x) {
+    Unit *a = reinterpret_cast<Unit *>(base + i * Tr::D);
+    Unit *b = reinterpret_cast<Unit *>(base + (n - 1 - i) * Tr::D);
+#pragma unroll
+    for (int w = 0; w < UPE; ++w) {
+      Unit x = a[w];
+      a[w] = b[w];
+      b[w] = x;
+    }
+  }
+}
+
+// ips4o_classify test kernel: the same tree_bucket the classification and
+// permutation kernels use.
+template <int DT>
+__global__ void classify_test_kernel(const char *elems, u64 n, const typename Traits<DT>::Key *tree,
+                                     const typename Traits<DT>::Key *spl, int l, int eq, u32 *out) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  __shared__ Key s_tree[256], s_spl[256];
+  for (int i = threadIdx.x; i < (1 << l); i += blockDim.x) {
+    s_tree[i] = tree[i];
+    s_spl[i] = spl[i];
+  }
+  __syncthreads();
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    out[i] = tree_bucket<Key>(s_tree, s_spl, l, eq, Tr::key(elems + i * Tr::D));
+}
+
+}  // namespace ips4o

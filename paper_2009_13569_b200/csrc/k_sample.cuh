@@ -1,0 +1,141 @@
+// k_sample.cuh -- K1: sampling phase + branchless splitter tree (P:719-737,
+// P:399-451, Fig. 2), one CTA per task; and the IPS2Ra digit setup
+// (P:1687-1696).
+#pragma once
+#include "common.cuh"
+
+namespace ips4o {
+
+constexpr int SAMPLE_THREADS = 512;
+template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 8192; }
+
+__host__ __device__ __forceinline__ int next_pow2_i(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+__host__ __device__ __forceinline__ int log2_i(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+// Ascending bitonic sort of a[0..P) in shared memory, P a power of two.
+template <class Key>
+__device__ void bitonic_sort_smem(Key *a, int P) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int p = i ^ j;
+        if (p > i) {
+          Key x = a[i], y = a[p];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Digit extractor setup for a task with key bounds [lo, hi] (IPS2Ra): all keys
+// share the bits above bitlen(lo ^ hi); the next log2(k) bits are the digit.
+template <class Key>
+__device__ __forceinline__ void digit_setup(LevelTask &L) {
+  Key lo = key_from_words<Key>(L.t.lo), hi = key_from_words<Key>(L.t.hi);
+  int h = bitlen((Key)(lo ^ hi));
+  int kb = log2_i((int)L.k_req);
+  int bits = h < kb ? h : kb;
+  L.l = bits;
+  L.shift = h - bits;
+  L.K = 1u << bits;
+  L.equality = 0;
+  L.k_used = 1u << bits;
+}
+
+// Trees are stored as [tree[0..KIDX) | splitter[0..KIDX)] per task.
+template <int DT, int ALGO>
+__global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  const int ti = blockIdx.x;
+  LevelTask &L = A.tasks[ti];
+  if (ALGO == ALGO_DIGIT) {
+    if (threadIdx.x == 0) digit_setup<Key>(L);
+    return;
+  }
+  extern __shared__ __align__(16) char smem_raw[];
+  Key *s_keys = reinterpret_cast<Key *>(smem_raw);
+  __shared__ Key s_cand[256];
+  __shared__ int s_u, s_leaves;
+  Key *tree = reinterpret_cast<Key *>(A.trees) + (size_t)ti * 2 * Tr::KIDX;
+  Key *spl = tree + Tr::KIDX;
+
+  const int m = (int)L.m;
+  const int P = next_pow2_i(m);
+  // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9)
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    Key v = key_max<Key>();
+    if (i < m) {
+      u64 idx = sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i);
+      v = Tr::key(A.base + idx * Tr::D);
+    }
+    s_keys[i] = v;
+  }
+  __syncthreads();
+  bitonic_sort_smem<Key>(s_keys, P);
+
+  if (threadIdx.x == 0) {
+    // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
+    // duplicate was removed (R23); R10: halve k until the indices fit.
+    int k = (int)L.k_req;
+    const int kidx_budget = (int)L.kidx;
+    for (;;) {
+      int alpha = m / k;
+      int u = 0, dup = 0;
+      for (int j = 0; j < k - 1; ++j) {
+        Key c = s_keys[(j + 1) * alpha - 1];
+        if (u > 0 && s_cand[u - 1] == c) {
+          dup = 1;
+          continue;
+        }
+        s_cand[u++] = c;
+      }
+      int leaves = next_pow2_i(u + 1);
+      int need = dup ? 2 * leaves : leaves;
+      if (need <= kidx_budget || k <= 2) {
+        L.K = (u32)need;
+        L.l = (u32)log2_i(leaves);
+        L.equality = (u32)dup;
+        L.k_used = (u32)k;
+        L.shift = 0;
+        s_u = u;
+        s_leaves = leaves;
+        break;
+      }
+      k >>= 1;
+    }
+  }
+  __syncthreads();
+  const int u = s_u, leaves = s_leaves, s = leaves - 1;
+  const int l = log2_i(leaves);
+  // pad with the largest splitter, splitter[s] = splitter[s-1]
+  for (int i = threadIdx.x; i < leaves; i += blockDim.x) spl[i] = s_cand[i < u ? i : u - 1];
+  // node i at depth d, position p holds in-order rank (2p+1)2^(l-1-d)-1
+  for (int i = threadIdx.x; i < leaves; i += blockDim.x) {
+    if (i == 0) {
+      tree[0] = (Key)0;
+      continue;
+    }
+    int d = 31 - __clz(i);
+    int p = i - (1 << d);
+    int rank = (2 * p + 1) * (1 << (l - 1 - d)) - 1;
+    tree[i] = s_cand[rank < u ? rank : u - 1];
+  }
+  (void)s;
+}
+
+}  // namespace ips4o

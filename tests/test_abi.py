@@ -1,0 +1,80 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every
+symbol include/ips4o.h declares; host-side argument validation (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "ips4o.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ips4o_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2009_13569_b200 import build
+
+    build.build()
+    import paper_2009_13569_b200 as p
+
+    return p.load()
+
+
+def test_header_declares_the_survey_entry_points():
+    fns = declared_functions()
+    for f in ["ips4o_sort", "ips4o_sort_ex", "ips4o_scratch_bytes", "ips4o_status_string"]:
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    import paper_2009_13569_b200 as p
+
+    for f in declared_functions():
+        assert hasattr(lib, f), f"{f} declared in include/ips4o.h but not exported"
+    assert set(declared_functions()) == set(p.EXPORTS)
+
+
+def test_built_for_sm100a():
+    import subprocess
+
+    from paper_2009_13569_b200 import build
+
+    so = build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_argument_validation_without_gpu(lib):
+    import paper_2009_13569_b200 as p
+
+    # n <= 1 returns 0 without device work
+    assert lib.ips4o_sort(None, 0, p.U64, None) == 0
+    assert lib.ips4o_sort(None, 1, p.U64, None) == 0
+    # unknown dtype, NULL pointer, misaligned pointer
+    assert lib.ips4o_sort(None, 10, 7, None) == -1
+    assert lib.ips4o_sort(None, 10, p.U64, None) == -1
+    assert lib.ips4o_sort(ctypes.c_void_p(8), 10, p.U64, None) == -1
+    assert lib.ips4o_sort(ctypes.c_void_p(16), 1 << 32, p.U64, None) == -1
+    assert lib.ips4o_status_string(-1).decode() == "invalid argument"
+    assert "sm_100" in lib.ips4o_status_string(-4).decode()
+
+
+def test_dtype_info_and_scratch_bound(lib):
+    import paper_2009_13569_b200 as p
+
+    for dt, D in p.ELEM_BYTES.items():
+        info = p.dtype_info(dt)
+        assert info["elem_bytes"] == D
+        # whole 32-byte sectors per block
+        assert (info["block_elems"] * D) % 32 == 0
+        assert info["kidx_max"] in (128, 256)
+        assert info["base_cap"] * D <= 200 * 1024
+    # scratch grows sub-linearly relative to the input (in-place)
+    n = 1 << 30
+    sb = p.scratch_bytes(n, p.U64)
+    assert 0 < sb < 0.15 * n * 8

@@ -1,0 +1,330 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance 0 (BASELINE.json north_star): U64/F64 byte-identical output; PAIR and
+REC100 identical key sequence and identical record multiset inside every run
+of equal keys (oracle.parity).  Sizes span several tiles, stripes and blocks
+with ragged tails; base_cap is lowered in some cases to force several
+partitioning levels at sizes the oracle finishes in seconds.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth_inputs as gen
+from gpu_util import (F64, PAIR, REC100, U64, from_dev, gpu_sort, key_bytes_of,
+                      splitters_as_elements, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ips():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2009_13569_b200 import build
+
+    build.build()
+    import paper_2009_13569_b200 as p
+
+    p.load()
+    return p
+
+
+def make(dtype, n, seed, kind="uniform"):
+    rng = np.random.default_rng(seed)
+    if dtype == U64:
+        if kind == "uniform":
+            return gen.uniform_u64(n, seed)
+        if kind == "dups":
+            return rng.integers(0, max(2, n // 16), n).astype(np.uint64)
+        if kind == "few":
+            return rng.integers(0, 3, n).astype(np.uint64)
+    if dtype == F64:
+        if kind == "uniform":
+            return gen.uniform_f64(n, seed)
+        if kind == "dups":
+            return np.round(gen.exponential_f64(n, seed), 2)
+        if kind == "few":
+            return rng.choice([-1.5, 0.0, 2.25], n)
+    if dtype == PAIR:
+        p = gen.pairs(n, seed)
+        if kind == "dups":
+            p[:, 0] = rng.integers(0, max(2, n // 16), n).astype(np.uint64)
+        if kind == "few":
+            p[:, 0] = rng.integers(0, 3, n).astype(np.uint64)
+        return p
+    r = gen.records100(n, seed)
+    if kind == "dups":
+        r[:, 2:10] = 0
+        r[:, 1] = r[:, 1] % 4
+    if kind == "few":
+        r[:, :10] = 0
+        r[:, 9] = rng.integers(0, 3, n).astype(np.uint8)
+    return r
+
+
+def check(orc, a, g, dtype):
+    o = orc.sort(a, dtype)
+    bad = orc.parity(g, o, dtype)
+    assert bad == -1, f"mismatch at index {bad} (n={a.shape[0] if a.ndim else a.size})"
+
+
+# ----------------------------------------------------------------- classifier
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("eq", [False, True])
+def test_device_classifier_matches_oracle(ips, orc, dtype, eq):
+    """The tree_bucket used by the classification/permutation kernels equals the
+    oracle's linear-scan definition P:432-437 on 10^4 elements."""
+    import torch
+
+    n = 10000
+    a = make(dtype, n, 3, "dups")
+    D = orc.ELEM_BYTES[dtype]
+    E = orc.elements(a, dtype)
+    idx = np.unique(np.random.default_rng(5).integers(0, n, 60))
+    sp = orc.sort(np.ascontiguousarray(E[idx]).reshape(-1), dtype).reshape(-1, D)
+    # unique splitters under the dtype order
+    uniq = [sp[0]]
+    for r in sp[1:]:
+        if orc.less(dtype, uniq[-1], r):
+            uniq.append(r)
+    uniq = np.stack(uniq)
+    u = uniq.shape[0]
+    raw = key_bytes_of(uniq.reshape(-1), dtype).tobytes()
+    tree, spl, l = orc.build_tree(uniq.reshape(-1), dtype)
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    ips.classify(to_dev(a), dtype, raw, u, eq, out)
+    got = out.cpu().numpy()
+    for i in range(0, n, 7):
+        want = orc.classify_linear(spl, l, eq, dtype, E[i])
+        assert got[i] == want, (i, got[i], want)
+
+
+# ----------------------------------------------------------------- one level
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("n,kind", [(5003, "uniform"), (100003, "uniform"), (70001, "dups"),
+                                    (40000, "few"), (1 << 20, "uniform")])
+def test_partition_step_tree(ips, orc, dtype, n, kind):
+    """K1..K5 of one level: the sampled tree is bit-identical to
+    the oracle's recomputation (same counter-based samples); E equals the
+    oracle histogram prefix; every element of [E_j, E_{j+1}) classifies to j;
+    each bucket holds exactly the oracle-sorted output restricted to it."""
+    if dtype == REC100 and n > 200000:
+        n = 200003
+    a = make(dtype, n, 11, kind)
+    t = to_dev(a)
+    info = ips.partition_step(t, dtype, base_cap=2048)
+    g = from_dev(t, a)
+    K, l, eq = info["num_buckets"], info["l"], info["equality"]
+    leaves = 1 << l
+    # K1 parity
+    st = orc.sample_tree(a, dtype, 0, n, info["seed"], 0, info["k_req"],
+                         info["samples"] // info["k_req"], info["kidx_budget"])
+    assert st["l"] == l and st["equality"] == eq and st["k"] == info["k_used"]
+    kb = info["key_bytes"]
+    D = orc.ELEM_BYTES[dtype]
+    o_tree = key_bytes_of(st["tree"], dtype).reshape(-1)
+    o_spl = key_bytes_of(st["splitter"], dtype).reshape(-1)
+    assert np.array_equal(info["splitter"], o_spl), "splitters differ from the oracle's"
+    assert np.array_equal(info["tree"][kb:], o_tree[kb:]), "tree differs from the oracle's"
+    assert K == (2 * leaves if eq else leaves)
+    # K3 parity: E equals the oracle histogram prefix with these splitters
+    spl_el = splitters_as_elements(info["splitter"], dtype, leaves)
+    hist = orc.histogram(a, dtype, spl_el, l, eq)
+    E = info["E"]
+    assert E[0] == 0 and E[-1] == n
+    assert np.array_equal(np.diff(E.astype(np.int64)), hist.astype(np.int64))
+    # K5 parity: bucket contents
+    o = orc.sort(a, dtype)
+    Ge = orc.elements(g, dtype)
+    Oe = orc.elements(o, dtype)
+    rng = np.random.default_rng(1)
+    for j in range(K):
+        e0, e1 = int(E[j]), int(E[j + 1])
+        if e1 == e0:
+            continue
+        probe = [e0, e1 - 1] + list(rng.integers(e0, e1, min(20, e1 - e0)))
+        for i in probe:
+            assert orc.classify_linear(spl_el, l, eq, dtype, Ge[i]) == j
+        seg = orc.sort(np.ascontiguousarray(Ge[e0:e1]).reshape(-1), dtype)
+        assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1, j
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("n", [5003, 300007])
+def test_partition_step_digit(ips, orc, dtype, n):
+    """IPS2Ra step: bucket j holds exactly the elements whose
+    digit (key >> shift) & (2^l - 1) is j, and the partition is consistent with
+    the oracle's sorted output."""
+    a = make(dtype, n, 12, "uniform")
+    t = to_dev(a)
+    info = ips.partition_step(t, dtype, algo=ips.DIGIT, base_cap=2048)
+    g = from_dev(t, a)
+    E = info["E"]
+    K, sh, bits = info["num_buckets"], info["shift"], info["l"]
+    assert K == 1 << bits and E[0] == 0 and E[-1] == n
+    Ge = orc.elements(g, dtype)
+    Oe = orc.elements(orc.sort(a, dtype), dtype)
+    for j in range(K):
+        e0, e1 = int(E[j]), int(E[j + 1])
+        for i in range(e0, e1, max(1, (e1 - e0) // 16)):
+            assert orc.radix_digit(dtype, Ge[i], sh, bits) == j
+        if e1 > e0:
+            seg = orc.sort(np.ascontiguousarray(Ge[e0:e1]).reshape(-1), dtype)
+            assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1
+
+
+# ----------------------------------------------------------------- full sorts
+SIZES = [0, 1, 2, 3, 31, 32, 33, 63, 64, 65, 4095, 4097, 24575, 24576, 24577, 49153, 100003]
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("n", SIZES)
+def test_sort_sizes(ips, orc, dtype, n):
+    a = make(dtype, n, n + 1, "uniform")
+    g, _ = gpu_sort(a, dtype)
+    check(orc, a, g, dtype)
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("kind", ["uniform", "dups", "few"])
+@pytest.mark.parametrize("base_cap", [300, 1024])
+def test_sort_deep_recursion(ips, orc, dtype, kind, base_cap):
+    """Small base capacity forces 2-4 partitioning levels at oracle-friendly n."""
+    n = 150001 if dtype != REC100 else 40001
+    a = make(dtype, n, 21, kind)
+    g, st = gpu_sort(a, dtype, base_cap=base_cap)
+    check(orc, a, g, dtype)
+    if kind == "uniform":
+        assert st["levels"] >= 2
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("kind", ["uniform", "dups", "few"])
+def test_sort_digit_algo(ips, orc, dtype, kind):
+    n = 200003 if dtype != REC100 else 50001
+    a = make(dtype, n, 31, kind)
+    g, st = gpu_sort(a, dtype, algo=ips.DIGIT, base_cap=1024)
+    check(orc, a, g, dtype)
+
+
+def _patterns(n, rng):
+    m = np.uint64(2**64 - 1)
+    u = gen.uniform_u64(n, 77)
+    pats = {
+        "all_equal": np.full(n, 42, dtype=np.uint64),
+        "one_min": np.concatenate([np.full(n - 1, 9, dtype=np.uint64), [np.uint64(0)]]),
+        "one_max": np.concatenate([np.full(n - 1, 9, dtype=np.uint64), [m]]),
+        "alternating": (np.arange(n) % 2).astype(np.uint64),
+        "many_max": np.where(rng.random(n) < 0.5, m, u).astype(np.uint64),
+        "extremes": np.where(rng.random(n) < 0.5, np.uint64(0), m).astype(np.uint64),
+        "k_distinct": (u % np.uint64(256)).astype(np.uint64),
+        "sorted": np.sort(u),
+        "reverse": np.sort(u)[::-1].copy(),
+        "one_swap": None,
+        "organ_pipe": np.concatenate([np.arange(n // 2), np.arange(n - n // 2)[::-1]]).astype(np.uint64),
+        "skew_one_bucket": np.where(rng.random(n) < 0.97, np.uint64(5), u).astype(np.uint64),
+        "zipf": gen.zipf_u64(n, 3),
+        "twodup": gen.twodup_u64(n),
+        "rootdup": gen.rootdup_u64(n),
+    }
+    s = np.sort(u)
+    i = n // 3
+    s[i], s[i + 1] = s[i + 1], s[i]
+    pats["one_swap"] = s
+    return pats
+
+
+@pytest.mark.parametrize("name", ["all_equal", "one_min", "one_max", "alternating", "many_max",
+                                  "extremes", "k_distinct", "sorted", "reverse", "one_swap",
+                                  "organ_pipe", "skew_one_bucket", "zipf", "twodup", "rootdup"])
+@pytest.mark.parametrize("base_cap", [0, 700])
+def test_sort_value_patterns(ips, orc, name, base_cap):
+    """SURVEY 8(c).3 value patterns (u64), default and forced recursion."""
+    n = 200003
+    a = _patterns(n, np.random.default_rng(9))[name]
+    g, st = gpu_sort(a, U64, base_cap=base_cap)
+    check(orc, a, g, U64)
+
+
+def test_easy_inputs_reported(ips, orc):
+    n = 100000
+    s = np.sort(gen.uniform_u64(n, 1))
+    g, st = gpu_sort(s, U64)
+    assert st["easy_input"] == 1 and np.array_equal(g, s)
+    g, st = gpu_sort(s[::-1].copy(), U64)
+    assert st["easy_input"] == 2 and np.array_equal(g, s)
+    g, st = gpu_sort(np.full(n, 3, dtype=np.uint64), U64)
+    assert st["easy_input"] == 3
+
+
+def test_f64_specials(ips, orc):
+    """Negative values, +-inf, subnormals, +-DBL_MAX, +0.0 (no -0.0, no NaN)."""
+    rng = np.random.default_rng(4)
+    special = np.array([-np.inf, np.inf, -1.7976931348623157e308, 1.7976931348623157e308,
+                        5e-324, -5e-324, 2.2250738585072014e-308, 0.0, -1.0, 1.0])
+    n = 120001
+    a = np.where(rng.random(n) < 0.3, special[rng.integers(0, special.size, n)],
+                 rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n))
+    a = a + 0.0
+    assert orc.check_input(a, F64) == -1
+    for bc in (0, 500):
+        g, _ = gpu_sort(a, F64, base_cap=bc)
+        check(orc, a, g, F64)
+
+
+def test_rec100_extras(ips, orc):
+    """Keys equal in bytes 0..8 differing in byte 9; keys differing only in
+    byte 0; payloads all distinct so multiset errors are visible."""
+    rng = np.random.default_rng(6)
+    n = 30001
+    r = gen.records100(n, 5)
+    r[: n // 2, :9] = 7
+    r[n // 2:, 1:10] = 0
+    for bc in (0, 300):
+        g, _ = gpu_sort(r, REC100, base_cap=bc)
+        check(orc, r, g, REC100)
+
+
+def test_scratch_is_reported_and_bounded(ips, orc):
+    n = 1 << 21
+    a = gen.uniform_u64(n, 2)
+    g, st = gpu_sort(a, U64)
+    assert 0 < st["scratch_bytes"] <= ips.scratch_bytes(n, U64)
+    check(orc, a, g, U64)
+
+
+def test_sort_host_end_to_end(ips, orc):
+    import torch
+
+    n = 300001
+    a = gen.uniform_u64(n, 8)
+    h = a.copy()
+    st = ips.sort_host(h, U64)          # pageable host memory -> staged copies
+    check(orc, a, h, U64)
+    pin = torch.from_numpy(a.view(np.int64).copy()).pin_memory()
+    ips.sort_host(pin, U64)             # pinned host memory -> direct copies
+    check(orc, a, pin.numpy().view(np.uint64), U64)
+
+
+def test_non_default_stream(ips, orc):
+    import torch
+
+    n = 250000
+    a = gen.uniform_u64(n, 12)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        t = to_dev(a)
+        ips.sort(t, U64)
+    s.synchronize()
+    check(orc, a, t.cpu().numpy().view(np.uint64), U64)
+
+
+def test_deterministic(ips):
+    a = gen.uniform_u64(1 << 20, 3)
+    g1, _ = gpu_sort(a, U64)
+    g2, _ = gpu_sort(a, U64)
+    assert np.array_equal(g1, g2)
