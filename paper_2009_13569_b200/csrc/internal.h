@@ -70,9 +70,11 @@ struct LevelArgs {
   u32 *counts;                // [stripe-bucket slot] elements per bucket per stripe
   u32 *pfill;                 // [stripe-bucket slot] elements left in partial buffers
   u32 *fullblocks;            // [nstripes] full blocks flushed per stripe
+  u32 *fcum;                  // [nstripes] exclusive prefix of fullblocks within the task
   char *partials;             // [stripe-bucket slot][b*D] partial buffer contents
   u64 *E;                     // [bucket_off + j], j <= K: exact boundaries (relative)
-  u32 *fblk;                  // [bucket_off + j]: full blocks of bucket j (task-wide)
+  u32 *fblk;                  // [bucket_off + j]: full block POSITIONS in region j after
+                              // classification (blocks of any bucket)
   u64 *wr;                    // [bucket_off + j] * 8 words: packed (w, r) at [0], readers at [4]
   char *overlap;              // [bucket_off + j][b*D] saved overlaps (cleanup phase a)
   char *overflow;             // [ntasks][b*D] overflow blocks
@@ -85,6 +87,8 @@ struct LevelArgs {
   u32 base_cap_tasks;
   u64 base_cap_elems;         // base-case capacity M (elements)
   u64 seed;
+  u32 dbg_one_agent;          // debug: a single permutation agent per task
+  u32 pad;
 };
 
 // The packed per-bucket permutation word: high 32

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -71,6 +72,7 @@ struct Ctx {
   int max_levels = 0;
   bool skip_prepass = false, skip_basecase = false;
   bool timing = false;
+  bool dbg_one_agent = false;  // IPS4O_DEBUG_ONE_AGENT=1: one permute CTA per task
   ips4o_stats *stats = nullptr;
   u64 launches = 0;
   u64 peak_scratch = 0;
@@ -165,6 +167,7 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.counts = ar.take<u32>(P.nsbk);
   A.pfill = ar.take<u32>(P.nsbk);
   A.fullblocks = ar.take<u32>(S);
+  A.fcum = ar.take<u32>(S);
   A.partials = ar.take<char>(P.nsbk * (size_t)B * D);
   A.E = ar.take<u64>(P.nbk);
   A.fblk = ar.take<u32>(P.nbk);
@@ -254,6 +257,7 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
     u64 nblocks = t.size / B;
     np = std::min<u64>(np, ceil_div(nblocks, (u64)PERM_WARPS * 2));
     np = std::max<u64>(np, 1);
+    if (c.dbg_one_agent) np = 1;
     L.perm_first = (u32)P.perm_task.size();
     L.nperm = (u32)np;
     for (u64 s = 0; s < np; ++s) P.perm_task.push_back((u32)i);
@@ -329,6 +333,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   A.algo = ALGO;
   A.seed = c.seed;
   A.base_cap_elems = c.base_cap;
+  A.dbg_one_agent = c.dbg_one_agent ? 1 : 0;
   // upload the plan (tasks, stripe->task, perm->task) through pinned staging
   const size_t T = P.lt.size(), S = P.stripe_task.size(), NP = P.perm_task.size();
   const size_t up = T * sizeof(LevelTask) + (S + NP) * 4 + 64;
@@ -361,7 +366,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CKLAUNCH();
   if ((rc = mark(c, KF_BOUND))) return rc;
   const size_t cum_smem = ((size_t)P.max_stripes_per_task + 1) * 4;
-  stripe_fix_kernel<DT><<<(unsigned)S, FIX_THREADS, cum_smem, c.st>>>(A);
+  stripe_fix_kernel<DT><<<(unsigned)S, FIX_THREADS, 0, c.st>>>(A);
   CKLAUNCH();
   if ((rc = mark(c, KF_FIX))) return rc;
   // K4 block permutation
@@ -622,6 +627,7 @@ static int init_ctx(Ctx &c, void *stream, const ips4o_options *opt, ips4o_stats 
   }
   c.stats = out;
   if (out) memset(out, 0, sizeof *out);
+  if (const char *e = getenv("IPS4O_DEBUG_ONE_AGENT")) c.dbg_one_agent = atoi(e) != 0;
   static bool pool_set = false;
   if (!pool_set) {
     // keep freed scratch in the pool between calls (setup amortisation,

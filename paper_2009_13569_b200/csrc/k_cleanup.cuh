@@ -33,16 +33,18 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
   char *gtask = A.base + L.t.begin * (u64)D;
   const u64 W = (A.wr[(bo + j) * WR_STRIDE] >> 32) * (u64)B;  // logical end of bucket j's blocks
   const u64 E1 = A.E[bo + j + 1];
+  const u64 d0 = (A.E[bo + j] + B - 1) / B * B;
+  const u64 o0 = E1 > d0 ? E1 : d0;  // bucket j's blocks cover [d0, W)
   auto logical = [&](u64 x) -> const Unit * {
     if (ovb == (u32)j && x >= pblk * B) return reinterpret_cast<const Unit *>(ovf + (x - pblk * B) * D);
     return reinterpret_cast<const Unit *>(gtask + x * D);
   };
-  if (W > E1) {
-    const u64 o = W - E1;  // < b
+  if (W > o0) {
+    const u64 o = W - o0;  // < b
     Unit *dst = reinterpret_cast<Unit *>(A.overlap + (bo + j) * (u64)B * D);
     for (u64 u = lane; u < o * UPE; u += 32) {
       u64 e = u / UPE, w = u % UPE;
-      dst[u] = logical(E1 + e)[w];
+      dst[u] = logical(o0 + e)[w];
     }
   }
   if (ovb == (u32)j) {
@@ -85,7 +87,8 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
   const u64 nhead = hd - E0;
   const u64 ntail = tl < E1 ? E1 - tl : 0;
   const u64 nholes = nhead + ntail;
-  const u64 o = W > E1 ? W - E1 : 0;    // saved overlap elements
+  const u64 o0 = E1 > d0 ? E1 : d0;
+  const u64 o = W > o0 ? W - o0 : 0;    // saved overlap elements
   const u32 nst = L.nstripes;
   u32 carry = 0;
   for (u32 base = 0; base < nst; base += FILL_THREADS) {

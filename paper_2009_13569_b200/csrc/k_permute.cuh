@@ -19,28 +19,47 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
   constexpr int KI = Tr::KIDX, B = Tr::B;
   static_assert(KI <= BND_THREADS, "one thread per bucket");
   __shared__ u32 ws[BND_THREADS / 32 + 1];
+  __shared__ u64 s_E[KI + 1];
   const u32 ti = blockIdx.x;
   LevelTask &L = A.tasks[ti];
   const int K = (int)L.K;
   const int j = threadIdx.x;
-  u32 c = 0, f = 0;
+  // prefix of the stripes' full-block counts (for F(x) below)
+  u32 carry = 0;
+  for (u32 b0 = 0; b0 < L.nstripes; b0 += BND_THREADS) {
+    u32 idx = b0 + threadIdx.x;
+    u32 v = idx < L.nstripes ? A.fullblocks[L.stripe_first + idx] : 0;
+    u32 tot;
+    u32 p = block_exclusive_scan<BND_THREADS>(v, ws, &tot);
+    if (idx < L.nstripes) A.fcum[L.stripe_first + idx] = carry + p;
+    carry += tot;
+  }
+  u32 c = 0;
   if (j < K) {
-    for (u32 s = 0; s < L.nstripes; ++s) {
-      const u64 slot = L.sbk_off + (u64)s * L.kidx + j;
-      u32 cs = A.counts[slot];
-      c += cs;
-      f += (cs - A.pfill[slot]) / B;
-    }
+    for (u32 s = 0; s < L.nstripes; ++s) c += A.counts[L.sbk_off + (u64)s * L.kidx + j];
   }
   u32 total;
   u32 pre = block_exclusive_scan<BND_THREADS>(c, ws, &total);
+  if (j < K) s_E[j] = pre;
+  if (j == 0) s_E[K] = L.t.size;
+  __syncthreads();
   const u64 bo = L.bucket_off;
   if (j < K) {
-    A.E[bo + j] = pre;
-    A.fblk[bo + j] = f;
-    u64 w = ((u64)pre + B - 1) / B;
-    i64 r = (i64)w + (i64)f - 1;
-    A.wr[(bo + j) * WR_STRIDE] = (w << 32) | (u64)(r + (i64)RBIAS);
+    // region j = blocks [ceil(E_j/b), ceil(E_{j+1}/b)); fr = full positions in it
+    const u64 SB = L.stripe_elems / B;
+    const u64 r0 = (s_E[j] + B - 1) / B, r1 = (s_E[j + 1] + B - 1) / B;
+    auto F = [&](u64 x) -> u64 {  // full block positions in [0, x)
+      u64 cc = x / SB;
+      if (cc >= L.nstripes) return carry;
+      u64 fb = A.fullblocks[L.stripe_first + cc];
+      u64 in = x - cc * SB;
+      return A.fcum[L.stripe_first + cc] + (in < fb ? in : fb);
+    };
+    const u64 fr = F(r1) - F(r0);
+    A.E[bo + j] = s_E[j];
+    A.fblk[bo + j] = (u32)fr;
+    const i64 r = (i64)r0 + (i64)fr - 1;
+    A.wr[(bo + j) * WR_STRIDE] = (r0 << 32) | (u64)(r + (i64)RBIAS);
     A.wr[(bo + j) * WR_STRIDE + 4] = 0;  // readers
   }
   if (j == 0) {
@@ -66,8 +85,6 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
   constexpr int D = Tr::D, B = Tr::B;
   constexpr int NU = B * D / (int)sizeof(Unit);
   constexpr int NWARPS = FIX_THREADS / 32;
-  extern __shared__ __align__(16) u32 s_cum[];  // [nstripes of task + 1]
-  __shared__ u32 ws[FIX_THREADS / 32 + 1];
   const u32 stripe = blockIdx.x;
   const u32 ti = A.stripe_task[stripe];
   const LevelTask &L = A.tasks[ti];
@@ -76,16 +93,34 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
   const u64 nblk_total = (L.t.size + B - 1) / B;     // incl. a partial last block
   const u64 c_lo = (u64)c * SB;
   const u64 c_hi = (c_lo + SB < nblk_total) ? c_lo + SB : nblk_total;
-  const u64 F = A.fullblocks[stripe];
-  const u64 e0 = c_lo + F;  // empty tail [e0, c_hi)
+  const u64 Fc = A.fullblocks[stripe];
+  const u64 e0 = c_lo + Fc;  // empty tail [e0, c_hi)
   if (e0 >= c_hi) return;
   const int K = (int)L.K;
   const u64 bo = L.bucket_off;
   char *gtask = A.base + L.t.begin * (u64)D;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 sf = L.stripe_first, nst = L.nstripes;
+  const u64 ftot = A.fcum[sf + nst - 1] + A.fullblocks[sf + nst - 1];
+  auto F = [&](u64 x) -> u64 {  // full block positions in [0, x) after classification
+    u64 cc = x / SB;
+    if (cc >= nst) return ftot;
+    u64 fb = A.fullblocks[sf + cc];
+    u64 in = x - cc * SB;
+    return A.fcum[sf + cc] + (in < fb ? in : fb);
+  };
+  auto select = [&](u64 q) -> u64 {  // position of the full block of rank q
+    u32 lo = 0, hi = nst;  // last stripe with fcum <= q
+    while (hi - lo > 1) {
+      u32 mid = (lo + hi) >> 1;
+      if (A.fcum[sf + mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    return (u64)lo * SB + (q - A.fcum[sf + lo]);
+  };
 
-  // first bucket whose prefix end d_j/b + f_j exceeds e0 (prefix ends are
-  // non-decreasing because bucket j's full blocks fit its region)
+  // first bucket whose prefix end r0_j + fr_j exceeds e0 (prefix ends are
+  // non-decreasing: region j's full positions fit region j)
   int jlo = 0, jhi = K;
   while (jlo < jhi) {
     int mid = (jlo + jhi) >> 1;
@@ -101,71 +136,20 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
     const u64 h0 = e0 > r0 ? e0 : r0;
     const u64 h1 = c_hi < pe ? c_hi : pe;
     if (h0 >= h1) continue;                          // no holes of j here
-    // stripes overlapping region [r0, r1)
-    const u64 ca = r0 / SB, cb = (r1 - 1) / SB;
-    const u32 nst = (u32)(cb - ca + 1);
-    // full positions of stripe cc within the region: [max(cc*SB, r0), min(cc*SB+F_cc, r1))
-    // (1) holes of bucket j before h0: (h0 - r0) - #full positions in [r0, h0)
-    // (2) sources (full positions >= pe) per stripe, cumulated from the LAST stripe
-    u32 before = 0;
-    for (u32 base = 0; base < nst; base += FIX_THREADS) {
-      u32 idx = base + threadIdx.x;
-      u32 srcs = 0, fb = 0;
-      if (idx < nst) {
-        u64 cc = ca + idx;
-        u64 f0 = cc * SB > r0 ? cc * SB : r0;
-        u64 fe = cc * SB + A.fullblocks[L.stripe_first + cc];
-        u64 f1 = fe < r1 ? fe : r1;
-        if (f1 > f0) {
-          u64 x1 = f1 < h0 ? f1 : h0;
-          fb = x1 > f0 ? (u32)(x1 - f0) : 0;           // full positions in [r0, h0)
-          u64 s0_ = f0 > pe ? f0 : pe;
-          srcs = f1 > s0_ ? (u32)(f1 - s0_) : 0;       // full positions in [pe, r1)
-        }
-      }
-      // store sources reversed so that a forward scan cumulates from the end
-      if (idx < nst) s_cum[nst - 1 - idx] = srcs;
-      u32 tot;
-      block_exclusive_scan<FIX_THREADS>(fb, ws, &tot);
-      before += tot;
-    }
-    __syncthreads();
-    // exclusive scan of s_cum[0..nst) in place (chunked)
-    u32 carry = 0;
-    for (u32 base = 0; base < nst; base += FIX_THREADS) {
-      u32 idx = base + threadIdx.x;
-      u32 v = idx < nst ? s_cum[idx] : 0;
-      u32 tot;
-      u32 p = block_exclusive_scan<FIX_THREADS>(v, ws, &tot);
-      if (idx < nst) s_cum[idx] = carry + p;
-      carry += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) s_cum[nst] = carry;
-    __syncthreads();
-    const u64 skip = (h0 - r0) - before;
+    // holes of region j before h0 belong to preceding stripes
+    const u64 skip = (h0 - r0) - (F(h0) - F(r0));
+    const u64 Fr1 = F(r1);
     const u64 nholes = h1 - h0;
-    // move: hole h0+i  <-  source number skip+i counted from the end
+    // hole h0+i <- the (skip+i)-th full block of region j counted from its end,
+    // i.e. the full block of task-wide rank Fr1 - 1 - (skip+i)
     for (u64 i = wid; i < nholes; i += NWARPS) {
-      const u32 g = (u32)(skip + i);
-      // reversed stripe index rr with s_cum[rr] <= g < s_cum[rr+1]
-      int lo = 0, hi = (int)nst;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (s_cum[mid] <= g) lo = mid + 1;
-        else hi = mid;
-      }
-      const int rr = lo - 1;
-      const u64 cc = ca + (nst - 1 - rr);
-      u64 fe = cc * SB + A.fullblocks[L.stripe_first + cc];
-      u64 f1 = fe < r1 ? fe : r1;
-      const u64 src = f1 - 1 - (g - s_cum[rr]);
+      const u64 q = Fr1 - 1 - (skip + i);
+      const u64 src = select(q);
       const u64 dstb = h0 + i;
       const Unit *s = reinterpret_cast<const Unit *>(gtask + src * B * D);
       Unit *d = reinterpret_cast<Unit *>(gtask + dstb * B * D);
       for (int u = lane; u < NU; u += 32) d[u] = s[u];
     }
-    __syncthreads();
   }
 }
 
@@ -212,13 +196,14 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   }
   __syncthreads();
   if (K <= 1) return;
+  if (A.dbg_one_agent && wid != 0) return;
   char *gtask = A.base + L.t.begin * (u64)D;
   const u64 size = L.t.size;
   const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow
   char *ovf = A.overflow + (size_t)ti * B * D;
   u64 *wr = A.wr + L.bucket_off * WR_STRIDE;
   const u32 agent = (cta - L.perm_first) * PERM_WARPS + wid;
-  const u32 nagents = L.nperm * PERM_WARPS;
+  const u32 nagents = A.dbg_one_agent ? 1 : L.nperm * PERM_WARPS;
   int p = (int)(((u64)agent * (u64)K) / nagents);  // P:847 starting points spread
 
   auto blk_ptr = [&](u64 x) -> Unit * {
@@ -314,8 +299,11 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
         dest = b2;
         continue;
       }
-      // empty block at w: wait until nobody reads from dest
+      // empty block at w: wait until nobody reads from dest.  The
+      // fence orders our RMW on (w, r) before the load of the reader count
+      // (a reader increments the count, fences, then RMWs (w, r)).
       if (lane == 0) {
+        __threadfence();
         while (ld_acquire_u64(&wr[(u64)dest * WR_STRIDE + 4]) != 0) __nanosleep(64);
       }
       __syncwarp();
