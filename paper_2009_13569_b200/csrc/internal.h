@@ -45,6 +45,7 @@ struct LevelTask {
   u32 pad0;
   u64 stripe_elems;  // elements per stripe (multiple of b); last stripe shorter
   u64 bucket_off;    // offset (in bucket slots) into per-task-bucket arrays
+  u64 blk_off;       // offset (in block slots) into the level's read-done flags
   u64 sbk_off;       // offset (in stripe-bucket slots) of this task's first stripe;
                      // stripe s uses slots [sbk_off + (s - stripe_first) * kidx, +kidx)
   // ---- results (device)
@@ -79,6 +80,7 @@ struct LevelArgs {
   char *overlap;              // [bucket_off + j][b*D] saved overlaps (cleanup phase a)
   char *overflow;             // [ntasks][b*D] overflow blocks
   u32 *ovf_used;              // [ntasks] bucket that wrote the overflow block, or ~0
+  unsigned char *rdone;       // [blk_off + x] block x of the task has been read (K4)
   // scheduler outputs
   TaskDesc *next_tasks;       // next level
   TaskDesc *base_tasks;       // base-case tasks of this level

@@ -149,6 +149,7 @@ struct LevelPlan {
   u32 max_m = 0;
   u64 nbk = 0;      // bucket slots
   u64 nsbk = 0;     // stripe-bucket slots
+  u64 nblk = 0;     // block slots (read-done flags)
   u64 child_cap = 0;
   u64 N = 0;
 };
@@ -175,6 +176,7 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.overlap = ar.take<char>(P.nbk * (size_t)B * D);
   A.overflow = ar.take<char>(T * (size_t)B * D);
   A.ovf_used = ar.take<u32>(T);
+  A.rdone = ar.take<unsigned char>(P.nblk);
   A.next_tasks = ar.take<TaskDesc>(P.child_cap);
   A.base_tasks = ar.take<TaskDesc>(P.child_cap);
   A.ntasks = (u32)T;
@@ -263,6 +265,8 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
     for (u64 s = 0; s < np; ++s) P.perm_task.push_back((u32)i);
     L.bucket_off = bo;
     bo += L.kidx + 1;
+    L.blk_off = P.nblk;
+    P.nblk += ceil_div(t.size, B) + 1;
     L.sbk_off = P.nsbk;
     P.nsbk += ns * L.kidx;
     P.child_cap += L.kidx;
@@ -347,6 +351,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CK(cudaMemcpyAsync((void *)A.stripe_task, hp + T * sizeof(LevelTask), S * 4, cudaMemcpyHostToDevice, c.st));
   CK(cudaMemcpyAsync((void *)A.perm_task, hp + T * sizeof(LevelTask) + S * 4, NP * 4, cudaMemcpyHostToDevice, c.st));
   CK(cudaMemsetAsync(A.counters, 0, 16 * 4, c.st));
+  CK(cudaMemsetAsync(A.rdone, 0, P.nblk, c.st));
   c.ms[KF_HOST] += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
 
   // K1 sampling + tree (or digit setup)

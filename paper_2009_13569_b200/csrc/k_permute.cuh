@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
     A.fblk[bo + j] = (u32)fr;
     const i64 r = (i64)r0 + (i64)fr - 1;
     A.wr[(bo + j) * WR_STRIDE] = (r0 << 32) | (u64)(r + (i64)RBIAS);
-    A.wr[(bo + j) * WR_STRIDE + 4] = 0;  // readers
+    A.wr[(bo + j) * WR_STRIDE + 1] = r0 + fr;  // prefix end (formerly full positions)
   }
   if (j == 0) {
     A.E[bo + K] = L.t.size;
@@ -156,21 +156,32 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
 // ------------------------------------------------------------------ K4
 // Block permutation.  Agents are warps; each holds its two swap
 // buffers in registers.  Per bucket a packed 64-bit word (w, r+RBIAS)
-// is read and modified with one atomic and a reader
-// counter implements "threads are only allowed to write to empty blocks if no
-// other threads are currently reading from the bucket".
+// is read and modified with ONE atomic, which gives every agent a consistent
+// view of both pointers.
+//
+// Reader tracking: a writer may fill an empty block only after the
+// agent that read that block (when w and r crossed) has finished reading it.
+// The paper counts readers per bucket; here every block position carries a
+// "read done" byte that the reader sets with a release store after its loads
+// completed, and a writer that targets a formerly full position waits on that
+// byte with acquire loads.  Same guarantee, no shared counters, no fences
+// (DESIGN "Permutation on the GPU").
 constexpr int PERM_WARPS = 8;
 constexpr int PERM_THREADS = PERM_WARPS * 32;
 
-template <int DT, int ALGO>
-__device__ __forceinline__ u32 classify_one(const typename Traits<DT>::Key *tree,
-                                            const typename Traits<DT>::Key *spl, int l, int eq,
-                                            int shift, u32 dmask, const char *e) {
-  using Key = typename Traits<DT>::Key;
-  Key k = Traits<DT>::key(e);
-  if (ALGO == ALGO_TREE) return tree_bucket<Key>(tree, spl, l, eq, k);
-  return digit_of(k, shift, dmask);
+__device__ __forceinline__ void st_release_u8(unsigned char *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_u8(const unsigned char *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class Unit> __device__ __forceinline__ u32 fold32(const Unit &u);
+template <> __device__ __forceinline__ u32 fold32<u64>(const u64 &u) { return (u32)u ^ (u32)(u >> 32); }
+template <> __device__ __forceinline__ u32 fold32<u32>(const u32 &u) { return u; }
+template <> __device__ __forceinline__ u32 fold32<uint4>(const uint4 &u) { return u.x ^ u.y ^ u.z ^ u.w; }
 
 template <int DT, int ALGO>
 __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
@@ -199,9 +210,10 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   if (A.dbg_one_agent && wid != 0) return;
   char *gtask = A.base + L.t.begin * (u64)D;
   const u64 size = L.t.size;
-  const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow
+  const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow (P:800-801)
   char *ovf = A.overflow + (size_t)ti * B * D;
   u64 *wr = A.wr + L.bucket_off * WR_STRIDE;
+  unsigned char *rdone = A.rdone + L.blk_off;
   const u32 agent = (cta - L.perm_first) * PERM_WARPS + wid;
   const u32 nagents = A.dbg_one_agent ? 1 : L.nperm * PERM_WARPS;
   int p = (int)(((u64)agent * (u64)K) / nagents);  // P:847 starting points spread
@@ -225,9 +237,21 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
       if (u < NU) d[u] = r[i];
     }
   };
-  auto first_bucket = [&](u64 x) -> u32 {
+  // bucket of the block held in registers: its key is in the first KEY_UNITS
+  // units, i.e. on lanes 0..KEY_UNITS-1 of register 0
+  auto bucket_of = [&](const Unit(&r)[NPL]) -> u32 {
+    Unit ku[Tr::KEY_UNITS];
+    if constexpr (Tr::KEY_UNITS == 1) {
+      ku[0] = r[0];
+    } else {
+#pragma unroll
+      for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = __shfl_sync(0xffffffffu, r[0], q);
+    }
     u32 b = 0;
-    if (lane == 0) b = classify_one<DT, ALGO>(s_tree, s_spl, l, eq, shift, dmask, (const char *)blk_ptr(x));
+    if (lane == 0) {
+      Key k = Tr::key(reinterpret_cast<const char *>(ku));
+      b = ALGO == ALGO_TREE ? tree_bucket<Key>(s_tree, s_spl, l, eq, k) : digit_of(k, shift, dmask);
+    }
     return __shfl_sync(0xffffffffu, b, 0);
   };
 
@@ -242,13 +266,10 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
         u64 cur = ld_relaxed_u64(&wr[(u64)p * WR_STRIDE]);
         i64 w = (i64)(cur >> 32), r = (i64)(cur & 0xFFFFFFFFull) - (i64)RBIAS;
         if (r >= w) {
-          atomicAdd(&wr[(u64)p * WR_STRIDE + 4], 1ull);
-          __threadfence();
           u64 old = atomicAdd(&wr[(u64)p * WR_STRIDE], ~0ull);  // r -= 1
           w = (i64)(old >> 32);
           r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
           if (r >= w) got = 1ull << 63 | (u64)r;
-          else atomicAdd(&wr[(u64)p * WR_STRIDE + 4], ~0ull);
         }
       }
       got = __shfl_sync(0xffffffffu, got, 0);
@@ -262,53 +283,45 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
     if (x == ~0ull) break;  // a whole cycle without work: done
     misses = 0;
     load_blk(x, buf0);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicAdd(&wr[(u64)p * WR_STRIDE + 4], ~0ull);  // reader done
-    u32 dest;
     {
-      // the key sits in the first KEY_UNITS units, i.e. on lanes 0..KEY_UNITS-1
-      Unit ku[Tr::KEY_UNITS];
-      if constexpr (Tr::KEY_UNITS == 1) {
-        ku[0] = buf0[0];
-      } else {
+      // every lane's loads have returned once the reduction has its operands;
+      // then publish "block x read" (release) for a writer waiting on it
+      u32 v = 0;
 #pragma unroll
-        for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = __shfl_sync(0xffffffffu, buf0[0], q);
-      }
-      u32 b = 0;
-      if (lane == 0) {
-        Key k = Tr::key(reinterpret_cast<const char *>(ku));
-        b = ALGO == ALGO_TREE ? tree_bucket<Key>(s_tree, s_spl, l, eq, k) : digit_of(k, shift, dmask);
-      }
-      dest = __shfl_sync(0xffffffffu, b, 0);
+      for (int i = 0; i < NPL; ++i) v ^= fold32<Unit>(buf0[i]);
+      v = __reduce_xor_sync(0xffffffffu, v);
+      asm volatile("" ::"r"(v));  // keep the dependency on every lane's loads
+      if (lane == 0) st_release_u8(rdone + x, 1u);
     }
-    // ---- place buf0 into dest, swapping as long as dest has unprocessed blocks
+    u32 dest = bucket_of(buf0);
+    // ---- place buf0 into dest, swapping while dest has unprocessed blocks
     for (;;) {
       u64 old = 0;
       if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
       old = __shfl_sync(0xffffffffu, old, 0);
       const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
       if (w <= r) {
-        // unprocessed block at w: skip it if it is already in place
-        u32 b2 = first_bucket((u64)w);
-        if (b2 == dest) continue;
+        // unprocessed block at w: swap, or skip it if already in place
         load_blk((u64)w, buf1);
+        const u32 b2 = bucket_of(buf1);
+        if (b2 == dest) continue;
         store_blk((u64)w, buf0);
 #pragma unroll
         for (int i = 0; i < NPL; ++i) buf0[i] = buf1[i];
         dest = b2;
         continue;
       }
-      // empty block at w: wait until nobody reads from dest.  The
-      // fence orders our RMW on (w, r) before the load of the reader count
-      // (a reader increments the count, fences, then RMWs (w, r)).
+      // empty block at w.  If it was full before the permutation, its
+      // reader must be done.
       if (lane == 0) {
-        __threadfence();
-        while (ld_acquire_u64(&wr[(u64)dest * WR_STRIDE + 4]) != 0) __nanosleep(64);
+        const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
+        if ((u64)w < pe) {
+          while (ld_acquire_u8(rdone + w) == 0) __nanosleep(32);
+        }
+        if ((u64)w == pblk) A.ovf_used[ti] = dest;
       }
       __syncwarp();
       store_blk((u64)w, buf0);
-      if ((u64)w == pblk && lane == 0) A.ovf_used[ti] = dest;
       break;
     }
   }
