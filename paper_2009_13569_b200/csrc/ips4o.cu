@@ -201,8 +201,13 @@ template <int DT> static int perm_occupancy() {
 template <int DT, int ALGO> static int set_attrs() {
   static bool done = false;
   if (done) return 0;
-  CK(cudaFuncSetAttribute(classify_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)ClsSmem<DT>::bytes));
+  if constexpr (DT == DT_REC100) {
+    CK(cudaFuncSetAttribute(classify_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ClsSmem<DT>::bytes));
+  } else {
+    CK(cudaFuncSetAttribute(classify_reg_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ClsReg<DT>::bytes));
+  }
   CK(cudaFuncSetAttribute(basecase_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)BaseSmem<DT>::bytes));
   CK(cudaFuncSetAttribute(sample_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -363,7 +368,11 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
     if ((rc = mark(c, KF_SAMPLE))) return rc;
   }
   // K2 classification + block flush
-  classify_kernel<DT, ALGO><<<(unsigned)S, Tr::CLS_THREADS, ClsSmem<DT>::bytes, c.st>>>(A);
+  if constexpr (DT == DT_REC100) {
+    classify_kernel<DT, ALGO><<<(unsigned)S, Tr::CLS_THREADS, ClsSmem<DT>::bytes, c.st>>>(A);
+  } else {
+    classify_reg_kernel<DT, ALGO><<<(unsigned)S, ClsReg<DT>::NT, ClsReg<DT>::bytes, c.st>>>(A);
+  }
   CKLAUNCH();
   if ((rc = mark(c, KF_CLASSIFY))) return rc;
   // K3 boundaries + stripe fix

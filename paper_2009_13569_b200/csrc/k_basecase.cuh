@@ -1,13 +1,15 @@
 // k_basecase.cuh -- K7: the base case, "small buckets are finished inside one
-// CTA in shared memory" (north star; P:980-982 and P:1652 use insertion sort
-// on CPUs).  One CTA per bucket of at most M elements:
+// CTA in shared memory" (north star; P:980-982, P:1652 use insertion sort on
+// CPUs).  One CTA per bucket of at most M elements:
 //   1. histogram of a digit of (key - lo) over the bucket's key bounds [lo,hi]
-//      (the bounds come from the splitters, so the digit splits the bucket
-//      into ~m/8 nearly equal runs),
-//   2. exclusive scan, scatter into shared memory (second, L2-resident read),
-//   3. sort every run: insertion sort for short runs (the paper's base case,
-//      P:1652), a warp bitonic network in shared memory for longer ones,
-//   4. coalesced write-back.
+//      (bounds come from the splitters, so the digit cuts the bucket into
+//      ~m/4 nearly equal runs),
+//   2. exclusive scan and scatter into shared memory (the second read of the
+//      bucket hits L2),
+//   3. runs longer than RANKMAX are sorted in place by a warp bitonic network,
+//   4. every element computes its rank inside its (short) run by counting the
+//      smaller elements -- the parallel form of the paper's insertion-sort
+//      base case -- and is written straight to its final global position.
 #pragma once
 #include "common.cuh"
 
@@ -18,7 +20,7 @@ template <int DT> struct BaseItem;
 template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 11, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 12, CAP = Traits<DT_U64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -27,7 +29,7 @@ template <> struct BaseItem<DT_U64> {
 template <> struct BaseItem<DT_F64> {
   using Item = u64;  // order-preserving key
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 11, CAP = Traits<DT_F64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 12, CAP = Traits<DT_F64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
   __device__ static Key key(const Item &it) { return it; }
@@ -39,7 +41,7 @@ struct alignas(16) PairItem {
 template <> struct BaseItem<DT_PAIR> {
   using Item = PairItem;
   using Key = u64;
-  static constexpr int THREADS = 512, DBMAX = 11, CAP = Traits<DT_PAIR>::BASE_CAP;
+  static constexpr int THREADS = 512, DBMAX = 12, CAP = Traits<DT_PAIR>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const PairItem *>(e); }
   __device__ static Key key(const Item &it) { return it.key; }
@@ -55,29 +57,19 @@ template <> struct BaseItem<DT_REC100> {
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
 };
 
+constexpr int RANKMAX = 32;  // longer runs are sorted by a warp bitonic network
+constexpr int BIGCAP = 1024;  // big runs handled per round
+
 template <int DT> struct BaseSmem {
   using BI = BaseItem<DT>;
   static constexpr size_t off_items = 0;
   static constexpr size_t off_rec = off_items + (size_t)BI::CAP * sizeof(typename BI::Item);
-  static constexpr size_t off_hist =
+  static constexpr size_t off_sidx =
       off_rec + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * Traits<DT>::D + 15) / 16 * 16 : 0);
+  static constexpr size_t off_hist = off_sidx + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * 2 + 15) / 16 * 16 : 0);
   static constexpr size_t off_big = off_hist + ((size_t)1 << BI::DBMAX) * 4;
-  static constexpr int BIGCAP = 1 << BI::DBMAX;
   static constexpr size_t bytes = off_big + (size_t)BIGCAP * 4 + (BI::THREADS / 32 + 4) * 4;
 };
-
-template <class BI>
-__device__ __forceinline__ void insertion_sort_run(typename BI::Item *a, int n) {
-  for (int i = 1; i < n; ++i) {
-    typename BI::Item x = a[i];
-    int j = i;
-    while (j > 0 && BI::less(x, a[j - 1])) {
-      a[j] = a[j - 1];
-      --j;
-    }
-    a[j] = x;
-  }
-}
 
 // Warp bitonic sort of a[0..n) in shared memory.  All comparators point the
 // same way (the "flip" form), so the virtual +inf padding to the next power of
@@ -90,12 +82,11 @@ __device__ void warp_bitonic_run(typename BI::Item *a, int n, int lane) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int q = lane; q < P / 2; q += 32) {
         int i, p;
+        int blk = q / j, off = q % j;
         if (j == (k >> 1)) {  // flip step
-          int blk = q / j, off = q % j;
           i = blk * k + off;
           p = blk * k + (k - 1 - off);
         } else {
-          int blk = q / j, off = q % j;
           i = blk * 2 * j + off;
           p = i + j;
         }
@@ -124,9 +115,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   extern __shared__ __align__(16) char smem[];
   Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
   char *s_rec = smem + S::off_rec;
+  unsigned short *s_sidx = reinterpret_cast<unsigned short *>(smem + S::off_sidx);
   u32 *s_hist = reinterpret_cast<u32 *>(smem + S::off_hist);
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
-  u32 *s_ws = s_big + S::BIGCAP;  // scan workspace (NT/32+1) + nbig
+  u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
   __shared__ u32 s_nbig;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
@@ -140,13 +132,13 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     if (m <= 1 || !(lo < hi)) continue;
     const int bits = bitlen((Key)(hi - lo));
     int db = 1;
-    while ((1 << (db + 3)) < m && db < BI::DBMAX) ++db;  // ~8 elements per digit
+    while ((1 << (db + 2)) < m && db < BI::DBMAX) ++db;  // ~4 elements per digit
     if (db > bits) db = bits;
     const int shift = bits - db;
     const int nd = (int)((hi - lo) >> shift) + 1;  // digits in use, <= 2^db
+    auto digit = [&](const Item &it) -> u32 { return (u32)((BI::key(it) - lo) >> shift); };
 
     for (int d = tid; d < nd; d += NT) s_hist[d] = 0;
-    if (tid == 0) s_nbig = 0;
     if constexpr (BI::STAGE_RECORDS) {
       // stage the records (coalesced u32 copy)
       const u32 *src = reinterpret_cast<const u32 *>(g);
@@ -157,12 +149,11 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     // 1. histogram
     for (int i = tid; i < m; i += NT) {
       const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
-      Item it = BI::load(e, (u32)i);
-      u32 d = (u32)((BI::key(it) - lo) >> shift);
-      atomicAdd(&s_hist[d], 1u);
+      atomicAdd(&s_hist[digit(BI::load(e, (u32)i))], 1u);
     }
     __syncthreads();
-    // 2. exclusive scan in place (chunked)
+    // 2. exclusive scan in place (chunked), then scatter; s_hist[d] becomes
+    //    the END of run d
     u32 carry = 0;
     for (int b0 = 0; b0 < nd; b0 += NT) {
       int d = b0 + tid;
@@ -173,50 +164,65 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       carry += tot;
     }
     __syncthreads();
-    // scatter (s_hist[d] becomes the END of run d)
     for (int i = tid; i < m; i += NT) {
       const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
       Item it = BI::load(e, (u32)i);
-      u32 d = (u32)((BI::key(it) - lo) >> shift);
-      u32 pos = atomicAdd(&s_hist[d], 1u);
+      u32 pos = atomicAdd(&s_hist[digit(it)], 1u);
       s_items[pos] = it;
     }
     __syncthreads();
-    // 3. sort the runs [end[d-1], end[d])
-    for (int d = tid; d < nd; d += NT) {
-      int a = d ? (int)s_hist[d - 1] : 0;
-      int n = (int)s_hist[d] - a;
-      if (n <= 1) continue;
-      if (shift == 0) continue;  // all keys of the run are equal
-      if (n <= 16) {
-        insertion_sort_run<BI>(s_items + a, n);
-      } else {
-        u32 slot = atomicAdd(&s_nbig, 1u);
-        s_big[slot] = (u32)d;
+    // 3. long runs: warp bitonic sort in place (rounds of BIGCAP runs)
+    if (shift > 0) {
+      for (int d0 = 0; d0 < nd; d0 += NT * 4) {
+        if (tid == 0) s_nbig = 0;
+        __syncthreads();
+        for (int d = d0 + tid; d < nd && d < d0 + NT * 4; d += NT) {
+          int a = d ? (int)s_hist[d - 1] : 0;
+          int n = (int)s_hist[d] - a;
+          if (n > RANKMAX) {
+            u32 slot = atomicAdd(&s_nbig, 1u);
+            if (slot < BIGCAP) s_big[slot] = (u32)d;
+          }
+        }
+        __syncthreads();
+        const int nbig = (int)(s_nbig < BIGCAP ? s_nbig : BIGCAP);
+        for (int q = wid; q < nbig; q += NT / 32) {
+          int d = (int)s_big[q];
+          int a = d ? (int)s_hist[d - 1] : 0;
+          warp_bitonic_run<BI>(s_items + a, (int)s_hist[d] - a, lane);
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
-    const int nbig = (int)s_nbig;
-    for (int q = wid; q < nbig; q += NT / 32) {
-      int d = (int)s_big[q];
-      int a = d ? (int)s_hist[d - 1] : 0;
-      int n = (int)s_hist[d] - a;
-      warp_bitonic_run<BI>(s_items + a, n, lane);
+    // 4. rank inside the run by counting, write to the final position
+    for (int i = tid; i < m; i += NT) {
+      const Item it = s_items[i];
+      const u32 d = digit(it);
+      const int a = d ? (int)s_hist[d - 1] : 0;
+      const int b = (int)s_hist[d];
+      int rank = i - a;
+      if (shift > 0 && b - a <= RANKMAX) {
+        rank = 0;
+        for (int j = a; j < b; ++j) {
+          const Item y = s_items[j];
+          rank += (BI::less(y, it) || (!BI::less(it, y) && j < i)) ? 1 : 0;
+        }
+      }
+      const int pos = a + rank;
+      if constexpr (DT == DT_U64 || DT == DT_PAIR) {
+        reinterpret_cast<Item *>(g)[pos] = it;
+      } else if constexpr (DT == DT_F64) {
+        reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
+      } else {
+        s_sidx[pos] = (unsigned short)(it & (Item)0xFFFF);
+      }
     }
-    __syncthreads();
-    // 4. write back
-    if constexpr (DT == DT_U64 || DT == DT_PAIR) {
-      Item *out = reinterpret_cast<Item *>(g);
-      for (int i = tid; i < m; i += NT) out[i] = s_items[i];
-    } else if constexpr (DT == DT_F64) {
-      u64 *out = reinterpret_cast<u64 *>(g);
-      for (int i = tid; i < m; i += NT) out[i] = key_to_f64((u64)BI::key(s_items[i]));
-    } else {
+    if constexpr (BI::STAGE_RECORDS) {
+      __syncthreads();
       // records: warp per record, lanes copy the 25 words
       u32 *out = reinterpret_cast<u32 *>(g);
       for (int i = wid; i < m; i += NT / 32) {
-        const u32 idx = (u32)(s_items[i] & (Item)0xFFFF);
-        const u32 *src = reinterpret_cast<const u32 *>(s_rec + (size_t)idx * D);
+        const u32 *src = reinterpret_cast<const u32 *>(s_rec + (size_t)s_sidx[i] * D);
         if (lane < D / 4) out[(size_t)i * (D / 4) + lane] = src[lane];
       }
     }

@@ -259,3 +259,210 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
 }
 
 }  // namespace ips4o
+
+namespace ips4o {
+
+// ------------------------------------------------------------------ K2, 8/16-byte elements
+// Same algorithm as classify_kernel, with the tile held in registers: each
+// thread owns RT_IPT elements of the tile (coalesced loads, the next tile is
+// prefetched into registers while the current one is classified), the tile
+// elements of emitted blocks are scattered into a shared staging array in
+// bucket order, and a block -> bucket map replaces per-block searches.
+template <int DT> struct ClsReg {
+  using Tr = Traits<DT>;
+  static constexpr int NT = 512;
+  static constexpr int T = Tr::D == 8 ? 4096 : 2048;
+  static constexpr int IPT = T / NT;
+  static constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX;
+  static constexpr int MAXBLK = T / B + KI;
+  static constexpr size_t off_buf = 0;
+  static constexpr size_t off_stage = off_buf + (size_t)KI * B * D;
+  static constexpr size_t off_tree = off_stage + (size_t)T * D;
+  static constexpr size_t off_u32 = off_tree + 2 * KI * sizeof(typename Tr::Key);
+  // u32 arrays: fill, tcnt, cnt, boff, eoff, nb (KI each) + ws (NT/32 + 1)
+  static constexpr size_t off_blkb = off_u32 + (6 * KI + NT / 32 + 1) * 4;
+  static constexpr size_t bytes = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
+};
+
+template <int DT>
+__device__ __forceinline__ typename Traits<DT>::Key elem_key(const typename Traits<DT>::Unit &x) {
+  if constexpr (DT == DT_PAIR) {
+    return ((u64)x.y << 32) | (u64)x.x;
+  } else if constexpr (DT == DT_F64) {
+    return f64_to_key(x);
+  } else {
+    return x;
+  }
+}
+
+template <int DT, int ALGO>
+__global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  using Unit = typename Tr::Unit;  // one element
+  using S = ClsReg<DT>;
+  constexpr int NT = S::NT, T = S::T, IPT = S::IPT, B = Tr::B, KI = Tr::KIDX;
+  constexpr int NWARPS = NT / 32;
+  static_assert(Tr::D == sizeof(Unit), "one unit per element");
+  static_assert(KI <= NT, "one thread per bucket in the scans");
+
+  extern __shared__ __align__(16) char smem[];
+  Unit *s_buf = reinterpret_cast<Unit *>(smem + S::off_buf);
+  Unit *s_stage = reinterpret_cast<Unit *>(smem + S::off_stage);
+  Key *s_tree = reinterpret_cast<Key *>(smem + S::off_tree);
+  Key *s_spl = s_tree + KI;
+  u32 *s_fill = reinterpret_cast<u32 *>(smem + S::off_u32);
+  u32 *s_tcnt = s_fill + KI;
+  u32 *s_cnt = s_tcnt + KI;
+  u32 *s_boff = s_cnt + KI;
+  u32 *s_eoff = s_boff + KI;
+  u32 *s_nb = s_eoff + KI;
+  u32 *s_ws = s_nb + KI;
+  unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 stripe = blockIdx.x;
+  const u32 ti = A.stripe_task[stripe];
+  const LevelTask &L = A.tasks[ti];
+  const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
+  const u32 dmask = L.K - 1;
+  const u64 size = L.t.size;
+  const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
+  const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
+  Unit *gtask = reinterpret_cast<Unit *>(A.base + L.t.begin * (u64)Tr::D);
+
+  if (ALGO == ALGO_TREE) {
+    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
+    for (int i = tid; i < (1 << l); i += NT) {
+      s_tree[i] = gt[i];
+      s_spl[i] = gt[KI + i];
+    }
+  }
+  for (int j = tid; j < KI; j += NT) {
+    s_tcnt[j] = 0;
+    s_cnt[j] = 0;
+    s_fill[j] = 0;
+  }
+  u32 myfill = 0;  // buffered elements of bucket tid (tid < KI)
+
+  const u64 n = s1 > s0 ? s1 - s0 : 0;
+  const u64 ntiles = (n + T - 1) / T;
+  u64 front = 0;
+  Unit x[IPT], y[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    u64 i = s0 + tid + (u64)k * NT;
+    if (i < s1) x[k] = gtask[i];
+  }
+  __syncthreads();
+
+  for (u64 t = 0; t < ntiles; ++t) {
+    const u64 e0 = s0 + t * T;
+    const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
+    // prefetch the next tile into registers
+    if (t + 1 < ntiles) {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) {
+        u64 i = e0 + T + tid + (u64)k * NT;
+        if (i < s1) y[k] = gtask[i];
+      }
+    }
+    // ---- classify (Alg. 1 batched over IPT elements)
+    u32 bkt[IPT], rank[IPT];
+    {
+      Key key[IPT];
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
+      if (ALGO == ALGO_TREE) {
+        tree_bucket_batch<Key, IPT>(s_tree, s_spl, l, eq, key, bkt);
+      } else {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) rank[k] = (tid + k * NT < cnt) ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;
+    __syncthreads();
+
+    // ---- per-bucket plan
+    u32 tc = 0, tot = 0, nb = 0, em = 0;
+    if (tid < KI) {
+      tc = s_tcnt[tid];
+      s_tcnt[tid] = 0;
+      s_fill[tid] = myfill;
+      tot = myfill + tc;
+      nb = tot / B;
+      em = nb ? nb * B - myfill : 0;
+    }
+    u32 total;
+    const u32 pre = block_exclusive_scan<NT>((nb << 16) | em, s_ws, &total);
+    if (tid < KI) {
+      const u32 bo = pre >> 16;
+      s_boff[tid] = bo;
+      s_eoff[tid] = pre & 0xFFFFu;
+      s_nb[tid] = nb;
+      s_cnt[tid] += tc;
+      for (u32 q = 0; q < nb; ++q) s_blkb[bo + q] = (unsigned short)tid;
+      myfill = tot - nb * B;
+    }
+    const u32 nblocks = total >> 16;
+    __syncthreads();
+
+    // ---- scatter the tile elements of emitted blocks in bucket order
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (tid + k * NT < cnt) {
+        const u32 j = bkt[k];
+        if (s_fill[j] + rank[k] < s_nb[j] * B) s_stage[s_eoff[j] + rank[k]] = x[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- emit full blocks to the stripe's write front (coalesced per warp)
+    for (u32 g = wid; g < nblocks; g += NWARPS) {
+      const u32 j = s_blkb[g];
+      const u32 q = g - s_boff[j];
+      const u32 bf = s_fill[j];
+      const u32 eo = s_eoff[j];
+      Unit *dst = gtask + s0 + (front + g) * B;
+#pragma unroll
+      for (int e = lane; e < B; e += 32) {
+        const u32 v = q * B + e;
+        dst[e] = v < bf ? s_buf[j * B + v] : s_stage[eo + v - bf];
+      }
+    }
+    front += nblocks;
+    __syncthreads();
+
+    // ---- remaining tile elements go to the (now free) buffer slots
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      if (tid + k * NT < cnt) {
+        const u32 j = bkt[k];
+        const u32 v = s_fill[j] + rank[k];
+        const u32 cut = s_nb[j] * B;
+        if (v >= cut) s_buf[j * B + (v - cut)] = x[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) x[k] = y[k];
+    __syncthreads();
+  }
+
+  // ---- outputs: counts, partial fill, full blocks, partial buffers
+  if (tid < KI) s_fill[tid] = myfill;
+  __syncthreads();
+  const u64 sbase = L.sbk_off + (u64)(stripe - L.stripe_first) * L.kidx;
+  for (int j = tid; j < (int)L.kidx; j += NT) {
+    A.counts[sbase + j] = s_cnt[j];
+    A.pfill[sbase + j] = s_fill[j];
+  }
+  if (tid == 0) A.fullblocks[stripe] = (u32)front;
+  for (int j = wid; j < K; j += NWARPS) {
+    const int f = (int)s_fill[j];
+    Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * Tr::D);
+    for (int u = lane; u < f; u += 32) dst[u] = s_buf[j * B + u];
+  }
+}
+
+}  // namespace ips4o
