@@ -281,7 +281,9 @@ template <int DT> struct ClsReg {
   static constexpr size_t off_u32 = off_tree + 2 * KI * sizeof(typename Tr::Key);
   // u32 arrays: fill, tcnt, cnt, boff, eoff, nb (KI each) + ws (NT/32 + 1)
   static constexpr size_t off_blkb = off_u32 + (6 * KI + NT / 32 + 1) * 4;
-  static constexpr size_t bytes = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
+  static constexpr int LUT_BITS = 11;
+  static constexpr size_t off_lut = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
+  static constexpr size_t bytes = off_lut + ((size_t)4 << LUT_BITS);
 };
 
 template <int DT>
@@ -319,6 +321,7 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
   u32 *s_nb = s_eoff + KI;
   u32 *s_ws = s_nb + KI;
   unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
+  u32 *s_lut = reinterpret_cast<u32 *>(smem + S::off_lut);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u32 stripe = blockIdx.x;
@@ -344,6 +347,38 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     s_fill[j] = 0;
   }
   u32 myfill = 0;  // buffered elements of bucket tid (tid < KI)
+
+  // Lookup table of starting leaves addressed by the most significant bits of
+  // (key - lo): slot q covers keys [lo + q*2^ls, lo + (q+1)*2^ls)
+  // and stores the leaves of its first and last key; the tree walk is then
+  // only needed between those leaves.  Exact: leaf = #{splitters < key}.
+  const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
+  int ls = bitlen((Key)(thi - tlo)) - S::LUT_BITS;
+  if (ls < 0) ls = 0;
+  const u32 nlut_used = (u32)((thi - tlo) >> ls) + 1;
+  const int nspl = (1 << l) - 1;  // s
+  if (ALGO == ALGO_TREE) {
+    __syncthreads();
+    auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
+      u32 a = 0, b = (u32)nspl;
+      while (a < b) {
+        u32 mid = (a + b) >> 1;
+        if (s_spl[mid] < v) a = mid + 1;
+        else b = mid;
+      }
+      return a;
+    };
+    for (u32 q = tid; q < (1u << S::LUT_BITS); q += NT) {
+      u32 e = 0;
+      if (q < nlut_used) {
+        const Key r0 = tlo + ((Key)q << ls);
+        const Key r1m = (thi - r0) < (((Key)1 << ls) - 1) ? thi : r0 + (((Key)1 << ls) - 1);
+        const u32 a = lower(r0), b = lower(r1m);
+        e = a | ((b - a) << 16);
+      }
+      s_lut[q] = e;
+    }
+  }
 
   const u64 n = s1 > s0 ? s1 - s0 : 0;
   const u64 ntiles = (n + T - 1) / T;
@@ -374,7 +409,22 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
 #pragma unroll
       for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
       if (ALGO == ALGO_TREE) {
-        tree_bucket_batch<Key, IPT>(s_tree, s_spl, l, eq, key, bkt);
+        u32 ent[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          u32 q = (u32)((key[k] - tlo) >> ls);
+          ent[k] = s_lut[q < nlut_used ? q : nlut_used - 1];
+        }
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          u32 a = ent[k] & 0xFFFFu, b = a + (ent[k] >> 16);
+          while (a < b) {  // lower bound inside the slot's leaf interval
+            u32 mid = (a + b) >> 1;
+            if (s_spl[mid] < key[k]) a = mid + 1;
+            else b = mid;
+          }
+          bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);

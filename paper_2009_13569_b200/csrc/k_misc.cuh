@@ -37,33 +37,45 @@ __device__ __forceinline__ u128 shfl_xor_key<u128>(u128 v, int m) {
   return ((u128)hi << 64) | lo;
 }
 
-// Each thread checks the adjacent pairs (i, i+1) of a grid-strided index set.
+// Each warp scans one contiguous segment in coalesced chunks of 32*PRE_UNROLL
+// elements; the right neighbour of element e comes from lane+1 by shuffle
+// (one direct load per chunk for the element after the chunk).
 template <int DT>
 __global__ void __launch_bounds__(PRE_THREADS) prepass_kernel(const char *base, u64 n, PrepassPart *parts) {
   using Tr = Traits<DT>;
   using Key = typename Tr::Key;
   constexpr int D = Tr::D;
+  constexpr int CH = 32 * PRE_UNROLL;
   u32 nd = 1, ni = 1;
   Key mn = key_max<Key>(), mx = (Key)0;
-  const u64 stride = (u64)gridDim.x * PRE_THREADS;
-  for (u64 i0 = (u64)blockIdx.x * PRE_THREADS + threadIdx.x; i0 < n; i0 += stride * PRE_UNROLL) {
-    Key a[PRE_UNROLL], b[PRE_UNROLL];
+  const int lane = threadIdx.x & 31;
+  const u64 gw = ((u64)blockIdx.x * PRE_THREADS + threadIdx.x) >> 5;
+  const u64 W = (u64)gridDim.x * PRE_THREADS / 32;
+  const u64 L = (n + W * CH - 1) / (W * CH) * CH;
+  const u64 b0 = gw * L;
+  const u64 b1 = b0 + L < n ? b0 + L : n;
+  for (u64 c = b0; c < b1; c += CH) {
+    Key k[PRE_UNROLL];
 #pragma unroll
     for (int u = 0; u < PRE_UNROLL; ++u) {
-      u64 i = i0 + (u64)u * stride;
-      if (i < n) {
-        a[u] = Tr::key(base + i * D);
-        b[u] = (i + 1 < n) ? Tr::key(base + (i + 1) * D) : a[u];
-      }
+      const u64 e = c + 32 * u + lane;
+      k[u] = e < b1 ? Tr::key(base + e * D) : (Key)0;
     }
 #pragma unroll
     for (int u = 0; u < PRE_UNROLL; ++u) {
-      u64 i = i0 + (u64)u * stride;
-      if (i < n) {
-        nd &= (a[u] <= b[u]) ? 1u : 0u;
-        ni &= (a[u] >= b[u]) ? 1u : 0u;
-        mn = a[u] < mn ? a[u] : mn;
-        mx = a[u] > mx ? a[u] : mx;
+      Key nx = shfl_key(k[u], (lane + 1) & 31);
+      const Key nx2 = shfl_key(k[u + 1 < PRE_UNROLL ? u + 1 : u], 0);
+      if (lane == 31) nx = nx2;
+      const u64 e = c + 32 * u + lane;
+      if (e < b1) {
+        const bool in_chunk = (32 * u + lane + 1 < CH) && (e + 1 < b1);
+        if (!in_chunk && e + 1 < n) nx = Tr::key(base + (e + 1) * D);
+        if (e + 1 < n) {
+          nd &= (k[u] <= nx) ? 1u : 0u;
+          ni &= (k[u] >= nx) ? 1u : 0u;
+        }
+        mn = k[u] < mn ? k[u] : mn;
+        mx = k[u] > mx ? k[u] : mx;
       }
     }
   }
@@ -77,7 +89,7 @@ __global__ void __launch_bounds__(PRE_THREADS) prepass_kernel(const char *base, 
   }
   __shared__ u32 s_nd[PRE_THREADS / 32], s_ni[PRE_THREADS / 32];
   __shared__ Key s_mn[PRE_THREADS / 32], s_mx[PRE_THREADS / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
   if (lane == 0) {
     s_nd[wid] = nd;
     s_ni[wid] = ni;
