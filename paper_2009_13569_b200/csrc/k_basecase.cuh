@@ -20,7 +20,7 @@ template <int DT> struct BaseItem;
 template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 12, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 13, CAP = Traits<DT_U64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -29,7 +29,7 @@ template <> struct BaseItem<DT_U64> {
 template <> struct BaseItem<DT_F64> {
   using Item = u64;  // order-preserving key
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 12, CAP = Traits<DT_F64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 13, CAP = Traits<DT_F64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
   __device__ static Key key(const Item &it) { return it; }
@@ -58,7 +58,7 @@ template <> struct BaseItem<DT_REC100> {
 };
 
 constexpr int RANKMAX = 32;  // longer runs are sorted by a warp bitonic network
-constexpr int BIGCAP = 1024;  // big runs handled per round
+constexpr int BIGCAP = 256;  // long runs listed per bucket (more: digit scan fallback)
 
 template <int DT> struct BaseSmem {
   using BI = BaseItem<DT>;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     if (m <= 1 || !(lo < hi)) continue;
     const int bits = bitlen((Key)(hi - lo));
     int db = 1;
-    while ((1 << (db + 2)) < m && db < BI::DBMAX) ++db;  // ~4 elements per digit
+    while ((1 << (db + 1)) < m && db < BI::DBMAX) ++db;  // ~2-4 elements per digit
     if (db > bits) db = bits;
     const int shift = bits - db;
     const int nd = (int)((hi - lo) >> shift) + 1;  // digits in use, <= 2^db
@@ -171,28 +171,35 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       s_items[pos] = it;
     }
     __syncthreads();
-    // 3. long runs: warp bitonic sort in place (rounds of BIGCAP runs)
+    // 3. long runs: warp bitonic sort in place.  Their list holds BIGCAP
+    //    entries; if there are more (a skewed bucket), warps scan the digits.
     if (shift > 0) {
-      for (int d0 = 0; d0 < nd; d0 += NT * 4) {
-        if (tid == 0) s_nbig = 0;
-        __syncthreads();
-        for (int d = d0 + tid; d < nd && d < d0 + NT * 4; d += NT) {
-          int a = d ? (int)s_hist[d - 1] : 0;
-          int n = (int)s_hist[d] - a;
-          if (n > RANKMAX) {
-            u32 slot = atomicAdd(&s_nbig, 1u);
-            if (slot < BIGCAP) s_big[slot] = (u32)d;
-          }
+      if (tid == 0) s_nbig = 0;
+      __syncthreads();
+      for (int d = tid; d < nd; d += NT) {
+        int a = d ? (int)s_hist[d - 1] : 0;
+        int n = (int)s_hist[d] - a;
+        if (n > RANKMAX) {
+          u32 slot = atomicAdd(&s_nbig, 1u);
+          if (slot < BIGCAP) s_big[slot] = (u32)d;
         }
-        __syncthreads();
-        const int nbig = (int)(s_nbig < BIGCAP ? s_nbig : BIGCAP);
+      }
+      __syncthreads();
+      const int nbig = (int)s_nbig;
+      if (nbig <= BIGCAP) {
         for (int q = wid; q < nbig; q += NT / 32) {
           int d = (int)s_big[q];
           int a = d ? (int)s_hist[d - 1] : 0;
           warp_bitonic_run<BI>(s_items + a, (int)s_hist[d] - a, lane);
         }
-        __syncthreads();
+      } else {
+        for (int d = wid; d < nd; d += NT / 32) {
+          int a = d ? (int)s_hist[d - 1] : 0;
+          int n = (int)s_hist[d] - a;
+          if (n > RANKMAX) warp_bitonic_run<BI>(s_items + a, n, lane);
+        }
       }
+      __syncthreads();
     }
     // 4. rank inside the run by counting, write to the final position
     for (int i = tid; i < m; i += NT) {

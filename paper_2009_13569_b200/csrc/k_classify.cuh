@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
   u32 *s_eoff = s_boff + KI;
   u32 *s_nb = s_eoff + KI;
   u32 *s_ws = s_nb + KI;
+  u64 *s_plan = reinterpret_cast<u64 *>(s_eoff);  // KI words over s_eoff/s_nb
   unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
   u32 *s_lut = reinterpret_cast<u32 *>(smem + S::off_lut);
 
@@ -434,23 +435,35 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     for (int k = 0; k < IPT; ++k) rank[k] = (tid + k * NT < cnt) ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;
     __syncthreads();
 
-    // ---- per-bucket plan
+    // ---- per-bucket plan: blocks to emit (nb) and tile elements they take
+    // (em); exclusive scan of (nb << 16 | em) with one barrier (each warp
+    // adds up the totals of the warps before it)
     u32 tc = 0, tot = 0, nb = 0, em = 0;
     if (tid < KI) {
       tc = s_tcnt[tid];
       s_tcnt[tid] = 0;
-      s_fill[tid] = myfill;
       tot = myfill + tc;
       nb = tot / B;
       em = nb ? nb * B - myfill : 0;
     }
-    u32 total;
-    const u32 pre = block_exclusive_scan<NT>((nb << 16) | em, s_ws, &total);
+    const u32 pv = (nb << 16) | em;
+    u32 incl = pv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 yv = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += yv;
+    }
+    if (lane == 31) s_ws[wid] = incl;
+    __syncthreads();
+    const u32 wv = lane < NWARPS ? s_ws[lane] : 0;
+    const u32 wpre = __reduce_add_sync(0xffffffffu, lane < wid ? wv : 0u);
+    const u32 total = __reduce_add_sync(0xffffffffu, wv);
     if (tid < KI) {
+      const u32 pre = wpre + incl - pv;
       const u32 bo = pre >> 16;
       s_boff[tid] = bo;
-      s_eoff[tid] = pre & 0xFFFFu;
-      s_nb[tid] = nb;
+      // plan word: fill | cut << 16 | eoff << 32
+      s_plan[tid] = (u64)myfill | ((u64)(nb * B) << 16) | ((u64)(pre & 0xFFFFu) << 32);
       s_cnt[tid] += tc;
       for (u32 q = 0; q < nb; ++q) s_blkb[bo + q] = (unsigned short)tid;
       myfill = tot - nb * B;
@@ -458,12 +471,19 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     const u32 nblocks = total >> 16;
     __syncthreads();
 
-    // ---- scatter the tile elements of emitted blocks in bucket order
+    // ---- scatter the tile elements of emitted blocks in bucket order; the
+    //      others remember their buffer slot
+    u32 slot[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
+      slot[k] = 0xFFFFFFFFu;
       if (tid + k * NT < cnt) {
         const u32 j = bkt[k];
-        if (s_fill[j] + rank[k] < s_nb[j] * B) s_stage[s_eoff[j] + rank[k]] = x[k];
+        const u64 pl = s_plan[j];
+        const u32 v = (u32)(pl & 0xFFFFu) + rank[k];
+        const u32 cut = (u32)(pl >> 16) & 0xFFFFu;
+        if (v < cut) s_stage[(u32)(pl >> 32) + rank[k]] = x[k];
+        else slot[k] = j * B + (v - cut);
       }
     }
     __syncthreads();
@@ -472,8 +492,9 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     for (u32 g = wid; g < nblocks; g += NWARPS) {
       const u32 j = s_blkb[g];
       const u32 q = g - s_boff[j];
-      const u32 bf = s_fill[j];
-      const u32 eo = s_eoff[j];
+      const u64 pl = s_plan[j];
+      const u32 bf = (u32)(pl & 0xFFFFu);
+      const u32 eo = (u32)(pl >> 32);
       Unit *dst = gtask + s0 + (front + g) * B;
 #pragma unroll
       for (int e = lane; e < B; e += 32) {
@@ -484,19 +505,15 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     front += nblocks;
     __syncthreads();
 
-    // ---- remaining tile elements go to the (now free) buffer slots
+    // ---- remaining tile elements go to the (now free) buffer slots.  No
+    //      barrier needed before the next tile: its first shared write that
+    //      conflicts (emission reading s_buf) comes after its barriers.
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      if (tid + k * NT < cnt) {
-        const u32 j = bkt[k];
-        const u32 v = s_fill[j] + rank[k];
-        const u32 cut = s_nb[j] * B;
-        if (v >= cut) s_buf[j * B + (v - cut)] = x[k];
-      }
+      if (slot[k] != 0xFFFFFFFFu) s_buf[slot[k]] = x[k];
     }
 #pragma unroll
     for (int k = 0; k < IPT; ++k) x[k] = y[k];
-    __syncthreads();
   }
 
   // ---- outputs: counts, partial fill, full blocks, partial buffers
