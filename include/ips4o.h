@@ -70,7 +70,7 @@ typedef struct ips4o_options {
                               power of two in [2, 256]; default per dtype            */
     uint64_t seed;         /* sampling seed (DESIGN R8); default 0x1F4A2C7            */
     int32_t alpha_min;     /* lower bound of the oversampling factor alpha; the paper
-                              uses alpha = 0.2 log2 n, default max(that, 32) */
+                              uses alpha = 0.2 log2 n, default max(that, 64) */
     int32_t base_cap;      /* base-case capacity M (elements per one-CTA sort);
                               default and maximum per dtype (DESIGN "Base case")      */
     int32_t max_levels;    /* stop after this many partitioning levels (debug);

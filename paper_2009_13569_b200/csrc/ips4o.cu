@@ -67,7 +67,7 @@ struct Ctx {
   int algo = ALGO_TREE;
   int k_max = 256;
   u64 seed = 0x1F4A2C7ull;
-  int alpha_min = 32;
+  int alpha_min = 64;
   u64 base_cap = 0;
   int max_levels = 0;
   bool skip_prepass = false, skip_basecase = false;

@@ -154,14 +154,20 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     __syncthreads();
     // 2. exclusive scan in place (chunked), then scatter; s_hist[d] becomes
     //    the END of run d
-    u32 carry = 0;
-    for (int b0 = 0; b0 < nd; b0 += NT) {
-      int d = b0 + tid;
-      u32 v = d < nd ? s_hist[d] : 0;
+    {
+      // blocked scan: thread tid owns digits [tid*per, (tid+1)*per)
+      const int per = (nd + NT - 1) / NT;
+      const int d0 = tid * per;
+      const int d1 = d0 + per < nd ? d0 + per : nd;
+      u32 sum = 0;
+      for (int d = d0; d < d1; ++d) sum += s_hist[d];
       u32 tot;
-      u32 p = block_exclusive_scan<NT>(v, s_ws, &tot);
-      if (d < nd) s_hist[d] = carry + p;
-      carry += tot;
+      u32 run = block_exclusive_scan<NT>(sum, s_ws, &tot);
+      for (int d = d0; d < d1; ++d) {
+        const u32 v = s_hist[d];
+        s_hist[d] = run;
+        run += v;
+      }
     }
     __syncthreads();
     for (int i = tid; i < m; i += NT) {

@@ -7,7 +7,7 @@
 namespace ips4o {
 
 constexpr int SAMPLE_THREADS = 512;
-template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 8192; }
+template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 16384; }
 
 __host__ __device__ __forceinline__ int next_pow2_i(int x) {
   int p = 1;
