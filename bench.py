@@ -35,7 +35,7 @@ ELEM = {0: 8, 1: 8, 2: 16, 3: 100}
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=30, help="log2 of the element count")
@@ -66,7 +66,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -291,7 +291,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = ncu_traffic()
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
-            "traffic": (traffic or {}).get(dom), "peak_source": peak_src,
+            "traffic": (traffic or {}).get(dom), "traffic_unit": "DRAM bytes per step (ncu, profiles/ncu_traffic.json)",
+            "peak_source": peak_src,
             "alg_bytes_per_step": alg[dom], "kernel_ms_per_step": km[dom]}
     # algorithmic whole-sort reading: 2 n D per partition level (+ base case)
     L_eff = elems_levels / n
