@@ -144,6 +144,21 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+// Bulk L2 prefetch of [p, p + bytes): a hint issued by threads tid < nthr in
+// 16 KiB pieces; the range is shrunk to whole 16-byte units inside it, so the
+// prefetch never touches memory outside [p, p + bytes).
+__device__ __forceinline__ void prefetch_l2(const void *p, u64 bytes, int tid, int nthr) {
+  uintptr_t a = ((uintptr_t)p + 15) & ~(uintptr_t)15;
+  uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)15;
+  if (e <= a) return;
+  constexpr u64 PIECE = 16384;
+  const u64 n = (u64)(e - a);
+  for (u64 off = (u64)tid * PIECE; off < n; off += (u64)nthr * PIECE) {
+    const u32 sz = (u32)((n - off) < PIECE ? (n - off) : PIECE);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + off), "r"(sz) : "memory");
+  }
+}
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }

@@ -124,10 +124,19 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
 
+  if (blockIdx.x < count) {
+    const TaskDesc t0 = tasks[blockIdx.x];
+    prefetch_l2(base + t0.begin * (u64)D, t0.size * (u64)D, tid, NT);
+  }
   for (u32 ti = blockIdx.x; ti < count; ti += gridDim.x) {
     const TaskDesc t = tasks[ti];
     const int m = (int)t.size;
     char *g = base + t.begin * (u64)D;
+    // the next bucket of this CTA streams into L2 while this one is sorted
+    if (ti + gridDim.x < count) {
+      const TaskDesc tn = tasks[ti + gridDim.x];
+      prefetch_l2(base + tn.begin * (u64)D, tn.size * (u64)D, tid, NT);
+    }
     const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
     if (m <= 1 || !(lo < hi)) continue;
     const int bits = bitlen((Key)(hi - lo));

@@ -395,7 +395,12 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
   for (u64 t = 0; t < ntiles; ++t) {
     const u64 e0 = s0 + t * T;
     const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
-    // prefetch the next tile into registers
+    // the tile after next streams into L2; the next tile goes into registers
+    if (t + 2 < ntiles) {
+      const u64 p0 = e0 + 2 * (u64)T;
+      const u64 p1 = p0 + T < s1 ? p0 + T : s1;
+      prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), tid, 2);
+    }
     if (t + 1 < ntiles) {
 #pragma unroll
       for (int k = 0; k < IPT; ++k) {
