@@ -13,9 +13,11 @@ typedef unsigned __int128 u128;
 enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3 };
 enum { ALGO_TREE = 0, ALGO_DIGIT = 1 };
 
-// Flags of a task / bucket.
+// Flags of a task.
 enum : u32 {
   TF_NONE = 0,
+  TF_MINMAX = 1,  // bounds unknown ([0, max]); K2 computes the key min/max and
+                  // K6 uses them for the children (the pre-pass was skipped)
 };
 
 // A task T[l, r): the subarray [begin, begin+size) of the input, with
@@ -55,6 +57,8 @@ struct LevelTask {
   int shift;         // digit shift (DIGIT)
   u32 k_used;        // k after the equality-budget rule (DESIGN R10)
   u32 pad1;
+  u64 lut_lo[2];     // key range of the sample (TREE): the classifier's lookup
+  u64 lut_hi[2];     // table spans [lut_lo, lut_hi] inside [t.lo, t.hi]
 };
 
 // Device pointers of one level's scratch arrays (all in one arena).
@@ -91,6 +95,7 @@ struct LevelArgs {
   u64 seed;
   u32 dbg_one_agent;          // debug: a single permutation agent per task
   u32 pad;
+  u64 *minmax;                // [0] = min key, [1] = max key of TF_MINMAX tasks (u64 keys)
 };
 
 // The packed per-bucket permutation word: high 32

@@ -177,6 +177,7 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.overflow = ar.take<char>(T * (size_t)B * D);
   A.ovf_used = ar.take<u32>(T);
   A.rdone = ar.take<unsigned char>(P.nblk);
+  A.minmax = ar.take<u64>(2);
   A.next_tasks = ar.take<TaskDesc>(P.child_cap);
   A.base_tasks = ar.take<TaskDesc>(P.child_cap);
   A.ntasks = (u32)T;
@@ -357,6 +358,8 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CK(cudaMemcpyAsync((void *)A.perm_task, hp + T * sizeof(LevelTask) + S * 4, NP * 4, cudaMemcpyHostToDevice, c.st));
   CK(cudaMemsetAsync(A.counters, 0, 16 * 4, c.st));
   CK(cudaMemsetAsync(A.rdone, 0, P.nblk, c.st));
+  CK(cudaMemsetAsync(A.minmax, 0xFF, 8, c.st));  // min = all ones
+  CK(cudaMemsetAsync(A.minmax + 1, 0, 8, c.st));  // max = 0
   c.ms[KF_HOST] += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
 
   // K1 sampling + tree (or digit setup)
@@ -468,15 +471,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   } else {
     next.clear();
   }
-  if (c.stats && !c.skip_basecase) {
-    // base-case elements of this level are tallied on the host from the list
-    // only in stats mode (cheap: one extra copy of the base list)
-    if (nbase) {
-      std::vector<TaskDesc> bl(nbase);
-      CK(cudaMemcpy(bl.data(), A.base_tasks, nbase * sizeof(TaskDesc), cudaMemcpyDeviceToHost));
-      for (auto &t : bl) c.stats->basecase_elems += t.size;
-    }
-  }
+  if (c.stats && !c.skip_basecase) c.stats->basecase_elems += (u64)hc[6] | ((u64)hc[7] << 32);
   CK(cudaFreeAsync(arena, c.st));
   return 0;
 }
@@ -550,7 +545,30 @@ static int sort_impl(Ctx &c, char *base, u64 n, StepCapture *cap) {
   root.size = n;
   key_to_words<Key>((Key)0, root.lo);
   key_to_words<Key>(key_max<Key>(), root.hi);
-  if (!c.skip_prepass || c.algo == ALGO_DIGIT || cap) {
+  bool need_prepass = !c.skip_prepass || c.algo == ALGO_DIGIT || cap;
+  if (need_prepass && !cap && !c.skip_prepass && c.algo == ALGO_TREE && sizeof(Key) == 8 &&
+      n > c.base_cap && n >= (1ull << 22)) {
+    // cheap sample pre-check: an ascending and a descending sampled pair
+    // prove the input is not an easy input; the key range then comes from K2
+    u32 *d = nullptr;
+    if (cudaMallocAsync((void **)&d, 256, c.st) != cudaSuccess) {
+      cudaGetLastError();
+      return IPS4O_ERR_NOMEM;
+    }
+    presample_kernel<DT><<<1, 1024, 0, c.st>>>(base, n, d);
+    CKLAUNCH();
+    if ((rc = ensure_pinned(c, 1 << 20))) return rc;
+    CK(cudaMemcpyAsync(c.pinned, d, 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaFreeAsync(d, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    const u32 *f = reinterpret_cast<const u32 *>(c.pinned);
+    if (f[0] && f[1]) {
+      need_prepass = false;
+      root.flags |= TF_MINMAX;
+    }
+    if ((rc = mark(c, KF_PRE))) return rc;
+  }
+  if (need_prepass) {
     PrepassOut po;
     if ((rc = run_prepass<DT>(c, base, n, &po))) return rc;
     Key mn = key_from_words<Key>(po.minkey), mx = key_from_words<Key>(po.maxkey);

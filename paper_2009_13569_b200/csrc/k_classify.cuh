@@ -350,13 +350,23 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
   u32 myfill = 0;  // buffered elements of bucket tid (tid < KI)
 
   // Lookup table of starting leaves addressed by the most significant bits of
-  // (key - lo): slot q covers keys [lo + q*2^ls, lo + (q+1)*2^ls)
-  // and stores the leaves of its first and last key; the tree walk is then
-  // only needed between those leaves.  Exact: leaf = #{splitters < key}.
+  // (key - llo), over the sample's key range [llo, lhi] inside
+  // the task bounds [tlo, thi]: slot q covers [llo + q*2^ls, llo + (q+1)*2^ls)
+  // (slot 0 extends down to tlo, the last slot up to thi) and stores the
+  // leaves of its first and last key; the search is then only needed between
+  // those leaves.  Exact: leaf = #{splitters < key}.
   const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
-  int ls = bitlen((Key)(thi - tlo)) - S::LUT_BITS;
+  Key llo = tlo, lhi = thi;
+  if (ALGO == ALGO_TREE) {
+    llo = key_from_words<Key>(L.lut_lo);
+    lhi = key_from_words<Key>(L.lut_hi);
+    if (llo < tlo) llo = tlo;
+    if (lhi > thi) lhi = thi;
+    if (lhi < llo) lhi = llo;
+  }
+  int ls = bitlen((Key)(lhi - llo)) - S::LUT_BITS;
   if (ls < 0) ls = 0;
-  const u32 nlut_used = (u32)((thi - tlo) >> ls) + 1;
+  const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
   const int nspl = (1 << l) - 1;  // s
   if (ALGO == ALGO_TREE) {
     __syncthreads();
@@ -372,14 +382,16 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     for (u32 q = tid; q < (1u << S::LUT_BITS); q += NT) {
       u32 e = 0;
       if (q < nlut_used) {
-        const Key r0 = tlo + ((Key)q << ls);
-        const Key r1m = (thi - r0) < (((Key)1 << ls) - 1) ? thi : r0 + (((Key)1 << ls) - 1);
-        const u32 a = lower(r0), b = lower(r1m);
+        const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
+        const Key r1 = q + 1 == nlut_used ? thi : llo + (((Key)(q + 1)) << ls) - 1;
+        const u32 a = lower(r0), b = lower(r1);
         e = a | ((b - a) << 16);
       }
       s_lut[q] = e;
     }
   }
+  const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
+  Key kmin = key_max<Key>(), kmax = (Key)0;
 
   const u64 n = s1 > s0 ? s1 - s0 : 0;
   const u64 ntiles = (n + T - 1) / T;
@@ -414,12 +426,22 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
       Key key[IPT];
 #pragma unroll
       for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
+      if (want_minmax) {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          if (tid + k * NT < cnt) {
+            kmin = key[k] < kmin ? key[k] : kmin;
+            kmax = key[k] > kmax ? key[k] : kmax;
+          }
+        }
+      }
       if (ALGO == ALGO_TREE) {
         u32 ent[IPT];
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
-          u32 q = (u32)((key[k] - tlo) >> ls);
-          ent[k] = s_lut[q < nlut_used ? q : nlut_used - 1];
+          const Key dk = key[k] - llo;
+          u32 q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
+          ent[k] = s_lut[q];
         }
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
@@ -534,6 +556,21 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
     const int f = (int)s_fill[j];
     Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * Tr::D);
     for (int u = lane; u < f; u += 32) dst[u] = s_buf[j * B + u];
+  }
+  if constexpr (sizeof(Key) == 8) {
+    if (want_minmax) {
+      // key range of the task, replacing the skipped pre-pass (TF_MINMAX)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Key a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+      }
+      if (lane == 0) {
+        atomicMin(reinterpret_cast<unsigned long long *>(&A.minmax[0]), (unsigned long long)kmin);
+        atomicMax(reinterpret_cast<unsigned long long *>(&A.minmax[1]), (unsigned long long)kmax);
+      }
+    }
   }
 }
 

@@ -149,7 +149,13 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
   const u32 ti = blockIdx.x;
   const LevelTask &L = A.tasks[ti];
   const int K = (int)L.K;
-  const Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
+  Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
+  if constexpr (sizeof(Key) == 8) {
+    if (L.t.flags & TF_MINMAX) {  // bounds measured by K2 (pre-pass skipped)
+      plo = (Key)A.minmax[0];
+      phi = (Key)A.minmax[1];
+    }
+  }
   const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
   const Key *spl = gt + KI;
   for (int j = threadIdx.x; j < K; j += SCHED_THREADS) {
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
     if (sz <= A.base_cap_elems) {
       u32 slot = atomicAdd(&A.counters[1], 1u);
       if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;
+      atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
     } else {
       u32 slot = atomicAdd(&A.counters[0], 1u);
       if (slot < A.next_cap) A.next_tasks[slot] = c;

@@ -133,6 +133,31 @@ __global__ void prepass_reduce_kernel(const PrepassPart *parts, int nparts, Prep
   key_to_words<Key>(mx, out->maxkey);
 }
 
+// Sample pre-check of the easy-input test (SURVEY 8(a) a0 "cheaper variant"):
+// 16384 stratified adjacent pairs.  If one pair ascends and another descends,
+// the input is neither sorted nor reverse-sorted (nor all equal) and the full
+// pre-pass can be skipped; otherwise the full pre-pass decides.
+constexpr int PRESAMPLE_PAIRS = 16384;
+
+template <int DT>
+__global__ void __launch_bounds__(1024) presample_kernel(const char *base, u64 n, u32 *out) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  int asc = 0, desc = 0;
+  for (int i = threadIdx.x; i < PRESAMPLE_PAIRS; i += blockDim.x) {
+    const u64 p = (u64)(((u128)(u64)i * (u128)(n - 1)) / (u128)PRESAMPLE_PAIRS);  // 0 .. n-2
+    const Key a = Tr::key(base + p * Tr::D), b = Tr::key(base + (p + 1) * Tr::D);
+    asc |= a < b;
+    desc |= b < a;
+  }
+  asc = __syncthreads_or(asc);
+  desc = __syncthreads_or(desc);
+  if (threadIdx.x == 0) {
+    out[0] = (u32)asc;
+    out[1] = (u32)desc;
+  }
+}
+
 // In-place reversal of n elements of D bytes ("reverses the input in
 // the case that the input was sorted in decreasing order").
 template <int DT>

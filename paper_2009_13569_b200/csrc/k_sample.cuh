@@ -89,6 +89,8 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   bitonic_sort_smem<Key>(s_keys, P);
 
   if (threadIdx.x == 0) {
+    key_to_words<Key>(s_keys[0], L.lut_lo);
+    key_to_words<Key>(s_keys[m - 1], L.lut_hi);
     // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
     // duplicate was removed (R23); R10: halve k until the indices fit.
     int k = (int)L.k_req;

@@ -250,6 +250,27 @@ def test_sort_value_patterns(ips, orc, name, base_cap):
     check(orc, a, g, U64)
 
 
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR])
+@pytest.mark.parametrize("kind", ["uniform", "dups", "few", "almost"])
+def test_sort_sample_precheck_path(ips, orc, dtype, kind):
+    """n >= 2^22: the sampled pre-check replaces the full pre-pass and the
+    level-1 classification measures the key range (TF_MINMAX); 'almost'
+    (sorted with a few swaps) usually sends it back to the full pre-pass."""
+    n = (1 << 22) + 3
+    if kind == "almost":
+        a = make(dtype, n, 41, "uniform")
+        if dtype == PAIR:
+            a = a[np.argsort(a[:, 0], kind="stable")]
+            a[[100, 101]] = a[[101, 100]]
+        else:
+            a = np.sort(a)
+            a[[n // 2, n // 2 + 1]] = a[[n // 2 + 1, n // 2]]
+    else:
+        a = make(dtype, n, 41, kind)
+    g, st = gpu_sort(a, dtype)
+    check(orc, a, g, dtype)
+
+
 def test_easy_inputs_reported(ips, orc):
     n = 100000
     s = np.sort(gen.uniform_u64(n, 1))
