@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", OUT, SRC, "-lrt", "-ldl", "-lpthread"]
+    extra = os.environ.get("IPS4O_EXTRA_NVCC_FLAGS", "").split()  # e.g. -DIPS4O_PHASE_TIMING
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT, SRC, "-lrt", "-ldl", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "lib", "build.log")
     with open(log, "w") as f:

@@ -103,6 +103,17 @@ __device__ void warp_bitonic_run(typename BI::Item *a, int n, int lane) {
   }
 }
 
+#ifdef IPS4O_PHASE_TIMING
+#define BC_PHASE(k)                                 \
+  if (tid == 0) {                                   \
+    long long now_ = clock64();                     \
+    ph_[k] += now_ - tprev_;                        \
+    tprev_ = now_;                                  \
+  }
+#else
+#define BC_PHASE(k)
+#endif
+
 template <int DT>
 __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap) {
@@ -123,6 +134,9 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
+#ifdef IPS4O_PHASE_TIMING
+  long long ph_[8] = {0}, tprev_ = clock64();
+#endif
 
   if (blockIdx.x < count) {
     const TaskDesc t0 = tasks[blockIdx.x];
@@ -155,12 +169,22 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       for (int w = tid; w < m * (D / 4); w += NT) dst[w] = src[w];
     }
     __syncthreads();
-    // 1. histogram
-    for (int i = tid; i < m; i += NT) {
-      const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
-      atomicAdd(&s_hist[digit(BI::load(e, (u32)i))], 1u);
+    BC_PHASE(0)
+    // 1. histogram (BU independent loads in flight per thread)
+    constexpr int BU = 8;
+    for (int i0 = tid; i0 < m; i0 += NT * BU) {
+      Item it[BU];
+#pragma unroll
+      for (int u = 0; u < BU; ++u) {
+        const int i = i0 + u * NT;
+        if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
+      }
+#pragma unroll
+      for (int u = 0; u < BU; ++u)
+        if (i0 + u * NT < m) atomicAdd(&s_hist[digit(it[u])], 1u);
     }
     __syncthreads();
+    BC_PHASE(1)
     // 2. exclusive scan in place (chunked), then scatter; s_hist[d] becomes
     //    the END of run d
     {
@@ -179,13 +203,24 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       }
     }
     __syncthreads();
-    for (int i = tid; i < m; i += NT) {
-      const char *e = BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D;
-      Item it = BI::load(e, (u32)i);
-      u32 pos = atomicAdd(&s_hist[digit(it)], 1u);
-      s_items[pos] = it;
+    BC_PHASE(2)
+    for (int i0 = tid; i0 < m; i0 += NT * BU) {
+      Item it[BU];
+#pragma unroll
+      for (int u = 0; u < BU; ++u) {
+        const int i = i0 + u * NT;
+        if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
+      }
+#pragma unroll
+      for (int u = 0; u < BU; ++u) {
+        if (i0 + u * NT < m) {
+          const u32 pos = atomicAdd(&s_hist[digit(it[u])], 1u);
+          s_items[pos] = it[u];
+        }
+      }
     }
     __syncthreads();
+    BC_PHASE(3)
     // 3. long runs: warp bitonic sort in place.  Their list holds BIGCAP
     //    entries; if there are more (a skewed bucket), warps scan the digits.
     if (shift > 0) {
@@ -216,7 +251,9 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       }
       __syncthreads();
     }
-    // 4. rank inside the run by counting, write to the final position
+    BC_PHASE(4)
+    // 4. rank inside the run by counting (independent compares, so warps keep
+    //    several loads in flight), write to the final position
     for (int i = tid; i < m; i += NT) {
       const Item it = s_items[i];
       const u32 d = digit(it);
@@ -249,7 +286,13 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       }
     }
     __syncthreads();
+    BC_PHASE(5)
   }
+#ifdef IPS4O_PHASE_TIMING
+  if (tid == 0 && blockIdx.x == 0)
+    printf("basecase CTA0 cycles: zero %lld hist %lld scan %lld scatter %lld big %lld rank+write %lld\n", ph_[0],
+           ph_[1], ph_[2], ph_[3], ph_[4], ph_[5]);
+#endif
 }
 
 }  // namespace ips4o
