@@ -44,7 +44,7 @@ def main():
         v = float(r[I["Metric Value"]].replace(",", ""))
         d[r[I["Metric Name"]]] = v
     ids = list(launches)
-    starts = [i for i in ids if "prepass_kernel" in launches[i]["name"]]
+    starts = [i for i in ids if re.search(r"presample_kernel|prepass_kernel", launches[i]["name"])]
     sel = ids[starts[-a.steps]:] if len(starts) >= a.steps else ids
     fam = defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_read": 0.0, "dram_write": 0.0})
     for i in sel:
