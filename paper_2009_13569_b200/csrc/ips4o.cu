@@ -364,7 +364,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
 
   // K1 sampling + tree (or digit setup)
   {
-    int pw = (int)next_pow2_u64(std::max<u32>(P.max_m, 1));
+    int pw = (int)next_pow2_u64(std::max<u32>(P.max_m, SORT_THREADS));
     size_t sm = ALGO == ALGO_TREE ? (size_t)pw * sizeof(Key) : 0;
     sample_kernel<DT, ALGO><<<(unsigned)T, SAMPLE_THREADS, sm, c.st>>>(A);
     CKLAUNCH();

@@ -1,9 +1,9 @@
 // k_basecase.cuh -- K7: the base case, "small buckets are finished inside one
 // CTA in shared memory" (north star; P:980-982, P:1652 use insertion sort on
 // CPUs).  One CTA per bucket of at most M elements:
-//   1. histogram of a digit of (key - lo) over the bucket's key bounds [lo,hi]
-//      (bounds come from the splitters, so the digit cuts the bucket into
-//      ~m/4 nearly equal runs),
+//   1. histogram of a digit of (key - lo) scaled to the bucket's key bounds
+//      [lo,hi] (bounds come from the splitters, so the digit cuts the bucket
+//      into ~m nearly equal runs of ~1 element; 16-bit counters),
 //   2. exclusive scan and scatter into shared memory (the second read of the
 //      bucket hits L2),
 //   3. runs longer than RANKMAX are sorted in place by a warp bitonic network,
@@ -20,7 +20,7 @@ template <int DT> struct BaseItem;
 template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 13, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 14, CAP = Traits<DT_U64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -29,7 +29,7 @@ template <> struct BaseItem<DT_U64> {
 template <> struct BaseItem<DT_F64> {
   using Item = u64;  // order-preserving key
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 13, CAP = Traits<DT_F64>::BASE_CAP;
+  static constexpr int THREADS = 1024, DBMAX = 14, CAP = Traits<DT_F64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
   __device__ static Key key(const Item &it) { return it; }
@@ -41,7 +41,7 @@ struct alignas(16) PairItem {
 template <> struct BaseItem<DT_PAIR> {
   using Item = PairItem;
   using Key = u64;
-  static constexpr int THREADS = 512, DBMAX = 12, CAP = Traits<DT_PAIR>::BASE_CAP;
+  static constexpr int THREADS = 512, DBMAX = 14, CAP = Traits<DT_PAIR>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const PairItem *>(e); }
   __device__ static Key key(const Item &it) { return it.key; }
@@ -50,7 +50,7 @@ template <> struct BaseItem<DT_PAIR> {
 template <> struct BaseItem<DT_REC100> {
   using Item = u128;  // key80 << 16 | index of the record in the staging area
   using Key = u128;
-  static constexpr int THREADS = 512, DBMAX = 9, CAP = Traits<DT_REC100>::BASE_CAP;
+  static constexpr int THREADS = 512, DBMAX = 11, CAP = Traits<DT_REC100>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = true;
   __device__ static Item load(const char *e, u32 idx) { return (Traits<DT_REC100>::key(e) << 16) | (u128)idx; }
   __device__ static Key key(const Item &it) { return it >> 16; }
@@ -67,7 +67,7 @@ template <int DT> struct BaseSmem {
   static constexpr size_t off_sidx =
       off_rec + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * Traits<DT>::D + 15) / 16 * 16 : 0);
   static constexpr size_t off_hist = off_sidx + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * 2 + 15) / 16 * 16 : 0);
-  static constexpr size_t off_big = off_hist + ((size_t)1 << BI::DBMAX) * 4;
+  static constexpr size_t off_big = off_hist + ((size_t)1 << BI::DBMAX) * 2;  // 16-bit counters, two per word
   static constexpr size_t bytes = off_big + (size_t)BIGCAP * 4 + (BI::THREADS / 32 + 4) * 4;
 };
 
@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
   __shared__ u32 s_nbig;
+  __shared__ u64 s_mul;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
@@ -153,15 +154,29 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
     const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
     if (m <= 1 || !(lo < hi)) continue;
-    const int bits = bitlen((Key)(hi - lo));
-    int db = 1;
-    while ((1 << (db + 1)) < m && db < BI::DBMAX) ++db;  // ~2-4 elements per digit
-    if (db > bits) db = bits;
-    const int shift = bits - db;
-    const int nd = (int)((hi - lo) >> shift) + 1;  // digits in use, <= 2^db
-    auto digit = [&](const Item &it) -> u32 { return (u32)((BI::key(it) - lo) >> shift); };
-
-    for (int d = tid; d < nd; d += NT) s_hist[d] = 0;
+    // digit(x) = floor(((x - lo) >> ds) * dmul / 2^64): monotone in x and
+    // spread evenly over nd digits, ~1 element per digit (nd = pow2 >= m).
+    // Key ranges narrower than nd use the offset itself (one key per digit).
+    int lg = 1;
+    while ((1 << lg) < m && lg < BI::DBMAX) ++lg;
+    const Key range = hi - lo;
+    const int bits = bitlen(range);
+    const int ds = bits > 64 ? bits - 64 : 0;
+    const u64 r64 = (u64)(range >> ds);
+    const bool direct = r64 < (1ull << lg);
+    const int nd = direct ? (int)r64 + 1 : (1 << lg);
+    const bool exact = direct && ds == 0;  // a digit holds a single key value
+    if (tid == 0) {
+      s_mul = direct ? 0ull
+                     : (r64 == ~0ull ? (1ull << lg) : (u64)(((u128)1 << (64 + lg)) / ((u128)r64 + 1)));
+    }
+    auto digit = [&](const Item &it) -> u32 {
+      const u64 v = (u64)((BI::key(it) - lo) >> ds);
+      return direct ? (u32)v : (u32)__umul64hi(v, s_mul);
+    };
+    const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
+    for (int w = tid; w < nw; w += NT) s_hist[w] = 0;
+    if (tid == 0) s_nbig = 0;
     if constexpr (BI::STAGE_RECORDS) {
       // stage the records (coalesced u32 copy)
       const u32 *src = reinterpret_cast<const u32 *>(g);
@@ -170,40 +185,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
     __syncthreads();
     BC_PHASE(0)
-    // 1. histogram (BU independent loads in flight per thread)
+    // 1. histogram of 16-bit counters (BU independent loads in flight)
     constexpr int BU = 8;
-    for (int i0 = tid; i0 < m; i0 += NT * BU) {
-      Item it[BU];
-#pragma unroll
-      for (int u = 0; u < BU; ++u) {
-        const int i = i0 + u * NT;
-        if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
-      }
-#pragma unroll
-      for (int u = 0; u < BU; ++u)
-        if (i0 + u * NT < m) atomicAdd(&s_hist[digit(it[u])], 1u);
-    }
-    __syncthreads();
-    BC_PHASE(1)
-    // 2. exclusive scan in place (chunked), then scatter; s_hist[d] becomes
-    //    the END of run d
-    {
-      // blocked scan: thread tid owns digits [tid*per, (tid+1)*per)
-      const int per = (nd + NT - 1) / NT;
-      const int d0 = tid * per;
-      const int d1 = d0 + per < nd ? d0 + per : nd;
-      u32 sum = 0;
-      for (int d = d0; d < d1; ++d) sum += s_hist[d];
-      u32 tot;
-      u32 run = block_exclusive_scan<NT>(sum, s_ws, &tot);
-      for (int d = d0; d < d1; ++d) {
-        const u32 v = s_hist[d];
-        s_hist[d] = run;
-        run += v;
-      }
-    }
-    __syncthreads();
-    BC_PHASE(2)
     for (int i0 = tid; i0 < m; i0 += NT * BU) {
       Item it[BU];
 #pragma unroll
@@ -214,53 +197,109 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #pragma unroll
       for (int u = 0; u < BU; ++u) {
         if (i0 + u * NT < m) {
-          const u32 pos = atomicAdd(&s_hist[digit(it[u])], 1u);
-          s_items[pos] = it[u];
+          const u32 d = digit(it[u]);
+          atomicAdd(&s_hist[d >> 1], 1u << ((d & 1) << 4));
+        }
+      }
+    }
+    __syncthreads();
+    BC_PHASE(1)
+    // 2. exclusive scan in place; warp w owns a contiguous chunk of words and
+    //    walks it 32 at a time.  Each word becomes (start(2w), start(2w+1)).
+    {
+      constexpr int NW = NT / 32;
+      const int chunk = ((nw + NW - 1) / NW + 31) & ~31;
+      const int c0 = wid * chunk, c1 = c0 + chunk < nw ? c0 + chunk : nw;
+      u32 part = 0;
+      for (int w = c0 + lane; w < c1; w += 32) {
+        const u32 h = s_hist[w];
+        part += (h & 0xFFFFu) + (h >> 16);
+      }
+      part = __reduce_add_sync(0xffffffffu, part);
+      if (lane == 0) s_ws[wid] = part;
+      __syncthreads();
+      u32 off = __reduce_add_sync(0xffffffffu, lane < wid ? s_ws[lane] : 0u);
+      for (int w0 = c0; w0 < c1; w0 += 32) {
+        const int w = w0 + lane;
+        const u32 h = w < c1 ? s_hist[w] : 0u;
+        const u32 v = (h & 0xFFFFu) + (h >> 16);
+        u32 x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const u32 st = off + x - v;
+        if (w < c1) {
+          s_hist[w] = st | ((st + (h & 0xFFFFu)) << 16);
+          // runs longer than RANKMAX are listed for the warp bitonic sort
+          if (!exact && v > RANKMAX) {
+            if ((h & 0xFFFFu) > RANKMAX) {
+              const u32 slot = atomicAdd(&s_nbig, 1u);
+              if (slot < BIGCAP) s_big[slot] = 2u * w;
+            }
+            if ((h >> 16) > RANKMAX) {
+              const u32 slot = atomicAdd(&s_nbig, 1u);
+              if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
+            }
+          }
+        }
+        off += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+    __syncthreads();
+    BC_PHASE(2)
+    // 3. scatter into shared memory in digit order (the second read of the
+    //    bucket hits L2); afterwards the counters hold the run ENDS
+    for (int i0 = tid; i0 < m; i0 += NT * BU) {
+      Item it[BU];
+#pragma unroll
+      for (int u = 0; u < BU; ++u) {
+        const int i = i0 + u * NT;
+        if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
+      }
+#pragma unroll
+      for (int u = 0; u < BU; ++u) {
+        if (i0 + u * NT < m) {
+          const u32 d = digit(it[u]);
+          const int sh = (d & 1) << 4;
+          const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
+          s_items[(old >> sh) & 0xFFFFu] = it[u];
         }
       }
     }
     __syncthreads();
     BC_PHASE(3)
-    // 3. long runs: warp bitonic sort in place.  Their list holds BIGCAP
+    const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // run ends
+    // 4. long runs: warp bitonic sort in place.  The list holds BIGCAP
     //    entries; if there are more (a skewed bucket), warps scan the digits.
-    if (shift > 0) {
-      if (tid == 0) s_nbig = 0;
-      __syncthreads();
-      for (int d = tid; d < nd; d += NT) {
-        int a = d ? (int)s_hist[d - 1] : 0;
-        int n = (int)s_hist[d] - a;
-        if (n > RANKMAX) {
-          u32 slot = atomicAdd(&s_nbig, 1u);
-          if (slot < BIGCAP) s_big[slot] = (u32)d;
-        }
-      }
-      __syncthreads();
+    if (!exact) {
       const int nbig = (int)s_nbig;
       if (nbig <= BIGCAP) {
         for (int q = wid; q < nbig; q += NT / 32) {
           int d = (int)s_big[q];
-          int a = d ? (int)s_hist[d - 1] : 0;
-          warp_bitonic_run<BI>(s_items + a, (int)s_hist[d] - a, lane);
+          int a = d ? (int)s_end[d - 1] : 0;
+          warp_bitonic_run<BI>(s_items + a, (int)s_end[d] - a, lane);
         }
       } else {
         for (int d = wid; d < nd; d += NT / 32) {
-          int a = d ? (int)s_hist[d - 1] : 0;
-          int n = (int)s_hist[d] - a;
+          int a = d ? (int)s_end[d - 1] : 0;
+          int n = (int)s_end[d] - a;
           if (n > RANKMAX) warp_bitonic_run<BI>(s_items + a, n, lane);
         }
       }
-      __syncthreads();
+      if (nbig) __syncthreads();
     }
     BC_PHASE(4)
-    // 4. rank inside the run by counting (independent compares, so warps keep
+    // 5. rank inside the run by counting (independent compares, so warps keep
     //    several loads in flight), write to the final position
     for (int i = tid; i < m; i += NT) {
       const Item it = s_items[i];
       const u32 d = digit(it);
-      const int a = d ? (int)s_hist[d - 1] : 0;
-      const int b = (int)s_hist[d];
+      const int a = d ? (int)s_end[d - 1] : 0;
+      const int b = (int)s_end[d];
       int rank = i - a;
-      if (shift > 0 && b - a <= RANKMAX) {
+      if (!exact && b - a > 1 && b - a <= RANKMAX) {
         rank = 0;
         for (int j = a; j < b; ++j) {
           const Item y = s_items[j];

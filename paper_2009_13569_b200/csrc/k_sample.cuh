@@ -6,7 +6,8 @@
 
 namespace ips4o {
 
-constexpr int SAMPLE_THREADS = 512;
+constexpr int SAMPLE_THREADS = 1024;  // = SORT_THREADS
+// at most 16 keys per thread of the register sort (4 for 16-byte keys)
 template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 16384; }
 
 __host__ __device__ __forceinline__ int next_pow2_i(int x) {
@@ -20,25 +21,86 @@ __host__ __device__ __forceinline__ int log2_i(int x) {
   return l;
 }
 
-// Ascending bitonic sort of a[0..P) in shared memory, P a power of two.
+// Ascending bitonic sort of the P = SORT_THREADS * E keys a[0..P) in shared
+// memory (Batcher's network, the same comparators as a plain smem bitonic
+// sort).  Thread t holds keys [t*E, (t+1)*E) in registers; compare-exchange
+// stages with stride j < E run inside the thread, E <= j < 32E across lanes
+// by shuffle, and only j >= 32E through shared memory (15 barrier-separated
+// stages at P = 16384 instead of 105).
+constexpr int SORT_THREADS = 1024;
+
 template <class Key>
-__device__ void bitonic_sort_smem(Key *a, int P) {
+__device__ __forceinline__ Key shfl_xor_k(Key v, int m) {
+  if constexpr (sizeof(Key) == 8) {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+  } else {
+    u64 lo = __shfl_xor_sync(0xffffffffu, (u64)v, m);
+    u64 hi = __shfl_xor_sync(0xffffffffu, (u64)(v >> 64), m);
+    return ((u128)hi << 64) | lo;
+  }
+}
+
+template <class Key, int E>
+__device__ void bitonic_sort_reg(Key *a) {
+  constexpr int P = SORT_THREADS * E;
+  const int t = threadIdx.x;
+  Key r[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) r[q] = a[t * E + q];
   for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        int p = i ^ j;
-        if (p > i) {
-          Key x = a[i], y = a[p];
-          bool up = (i & k) == 0;
+    if (k / 2 >= 32 * E) {
+      // strides that cross warps: through shared memory
+#pragma unroll
+      for (int q = 0; q < E; ++q) a[t * E + q] = r[q];
+      __syncthreads();
+      for (int j = k >> 1; j >= 32 * E; j >>= 1) {
+        for (int i = t; i < P; i += SORT_THREADS) {
+          const int p = i ^ j;
+          if (p > i) {
+            Key x = a[i], y = a[p];
+            if ((x > y) == ((i & k) == 0)) {
+              a[i] = y;
+              a[p] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < E; ++q) r[q] = a[t * E + q];
+    }
+    // strides E <= j < 32E: partner on lane ^ (j / E), same register
+    for (int j = (k >> 1) < 32 * E ? (k >> 1) : 16 * E; j >= E; j >>= 1) {
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int i = t * E + q;
+        const Key o = shfl_xor_k<Key>(r[q], j / E);
+        const bool lower = (i & j) == 0, up = (i & k) == 0;
+        const bool take_min = lower == up;
+        r[q] = take_min ? (o < r[q] ? o : r[q]) : (o > r[q] ? o : r[q]);
+      }
+    }
+    // strides j < E: inside the thread
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {
+      if (j >= k) continue;
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        if ((q & j) == 0) {
+          const int i = t * E + q;
+          const bool up = (i & k) == 0;
+          Key x = r[q], y = r[q | j];
           if ((x > y) == up) {
-            a[i] = y;
-            a[p] = x;
+            r[q] = y;
+            r[q | j] = x;
           }
         }
       }
-      __syncthreads();
     }
   }
+#pragma unroll
+  for (int q = 0; q < E; ++q) a[t * E + q] = r[q];
+  __syncthreads();
 }
 
 // Digit extractor setup for a task with key bounds [lo, hi] (IPS2Ra): all keys
@@ -75,7 +137,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   Key *spl = tree + Tr::KIDX;
 
   const int m = (int)L.m;
-  const int P = next_pow2_i(m);
+  const int P = next_pow2_i(m) > SORT_THREADS ? next_pow2_i(m) : SORT_THREADS;
   // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9)
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
     Key v = key_max<Key>();
@@ -86,7 +148,17 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
     s_keys[i] = v;
   }
   __syncthreads();
-  bitonic_sort_smem<Key>(s_keys, P);
+  switch (P / SORT_THREADS) {
+    case 1: bitonic_sort_reg<Key, 1>(s_keys); break;
+    case 2: bitonic_sort_reg<Key, 2>(s_keys); break;
+    case 4: bitonic_sort_reg<Key, 4>(s_keys); break;
+    default:
+      if constexpr (sizeof(Key) == 8) {
+        if (P == 8 * SORT_THREADS) bitonic_sort_reg<Key, 8>(s_keys);
+        else bitonic_sort_reg<Key, 16>(s_keys);
+      }
+      break;
+  }
 
   if (threadIdx.x == 0) {
     key_to_words<Key>(s_keys[0], L.lut_lo);
