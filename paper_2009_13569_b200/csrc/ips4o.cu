@@ -206,8 +206,8 @@ template <int DT, int ALGO> static int set_attrs() {
     CK(cudaFuncSetAttribute(classify_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ClsSmem<DT>::bytes));
   } else {
-    CK(cudaFuncSetAttribute(classify_reg_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)ClsReg<DT>::bytes));
+    CK(cudaFuncSetAttribute(classify_v2_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)ClsV2<DT>::bytes));
   }
   CK(cudaFuncSetAttribute(basecase_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)BaseSmem<DT>::bytes));
@@ -231,7 +231,8 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
   u64 se = round_up(ceil_div(P.N, target_stripes), B);
   se = std::max<u64>(se, round_up((u64)Tr::CLS_TILE * 2, B));
   const int occ = perm_occupancy<DT>();
-  const u64 G_perm = (u64)c.sms * occ;
+  u64 G_perm = (u64)c.sms * occ;
+  if (const char *e = getenv("IPS4O_PERM_CTAS_PER_SM")) G_perm = (u64)c.sms * (u64)std::max(1, atoi(e));  // tuning
   P.lt.resize(tasks.size());
   u64 bo = 0;
   for (size_t i = 0; i < tasks.size(); ++i) {
@@ -374,7 +375,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   if constexpr (DT == DT_REC100) {
     classify_kernel<DT, ALGO><<<(unsigned)S, Tr::CLS_THREADS, ClsSmem<DT>::bytes, c.st>>>(A);
   } else {
-    classify_reg_kernel<DT, ALGO><<<(unsigned)S, ClsReg<DT>::NT, ClsReg<DT>::bytes, c.st>>>(A);
+    classify_v2_kernel<DT, ALGO><<<(unsigned)S, ClsV2<DT>::NT, ClsV2<DT>::bytes, c.st>>>(A);
   }
   CKLAUNCH();
   if ((rc = mark(c, KF_CLASSIFY))) return rc;
@@ -387,8 +388,38 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CKLAUNCH();
   if ((rc = mark(c, KF_FIX))) return rc;
   // K4 block permutation
+#ifdef IPS4O_PERM_CLOCKS
+  {
+    unsigned long long z[6] = {0};
+    CK(cudaMemcpyToSymbolAsync(g_perm_clk, z, sizeof z, 0, cudaMemcpyHostToDevice, c.st));
+  }
+#endif
+#ifdef IPS4O_PERM_STATS
+  {
+    unsigned long long z[8] = {0};
+    CK(cudaMemcpyToSymbolAsync(g_perm_stats, z, sizeof z, 0, cudaMemcpyHostToDevice, c.st));
+  }
+#endif
   permute_kernel<DT, ALGO><<<(unsigned)NP, PERM_THREADS, 0, c.st>>>(A);
   CKLAUNCH();
+#ifdef IPS4O_PERM_CLOCKS
+  {
+    unsigned long long z[6];
+    CK(cudaMemcpyFromSymbolAsync(z, g_perm_clk, sizeof z, 0, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    fprintf(stderr, "permute L%d cycles/step: fetch %.0f atomic %.0f load %.0f emptywait %.0f  (steps %llu)\n", level_no,
+            (double)z[0] / z[4], (double)z[1] / z[4], (double)z[2] / z[4], (double)z[3] / z[4], z[4]);
+  }
+#endif
+#ifdef IPS4O_PERM_STATS
+  {
+    unsigned long long z[8];
+    CK(cudaMemcpyFromSymbolAsync(z, g_perm_stats, sizeof z, 0, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    fprintf(stderr, "permute L%d: attempts %llu fetches %llu misses %llu swaps %llu skips %llu empty %llu waits %llu polls %llu\n",
+            level_no, z[0], z[1], z[2], z[3], z[4], z[5], z[6], z[7]);
+  }
+#endif
   if ((rc = mark(c, KF_PERM))) return rc;
   // K5 cleanup
   cleanup_save_kernel<DT><<<dim3((KI + CLN_WARPS - 1) / CLN_WARPS, (unsigned)T), CLN_WARPS * 32, 0, c.st>>>(A);

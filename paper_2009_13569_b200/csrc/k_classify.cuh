@@ -575,3 +575,332 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
 }
 
 }  // namespace ips4o
+
+namespace ips4o {
+
+// ------------------------------------------------------------------ K2 v2, 8/16-byte elements
+// Tile-synchronous classification with block buffers, three barriers per tile.
+// 1024 threads; each owns IPT elements of a T-element tile in registers (the
+// next tile is loaded while the current one is processed).  Per tile:
+//   classify (LUT of starting leaves + short search) and rank by
+//   shared atomics  | A |  the previous tile's leftovers enter the freed
+//   buffers; one scan over the k' buckets plans, per bucket j, nb_j full
+//   blocks: block 0 is buffer j completed by the first B - fill_j tile
+//   elements, blocks 1..nb_j-1 are whole runs of tile elements staged
+//   contiguously; the remaining elements are leftovers  | B |  scatter: every
+//   element is stored once, into buffer j, its staged block, or kept in
+//   registers as a leftover  | C |  warps copy the emitted blocks to the
+//   stripe's write front.  Leftovers are written into buffer j
+//   after the next tile's barrier A, once the copies have read buffer j.
+template <int DT> struct ClsV2 {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+#ifndef IPS4O_CLS_NT
+#define IPS4O_CLS_NT 1024
+#endif
+  static constexpr int NT = IPS4O_CLS_NT;
+  static constexpr int T = Tr::D == 8 ? 4096 : 2048;
+  static constexpr int IPT = T / NT;
+  static constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX;
+  static constexpr int BUFS = B + (Tr::D == 8 ? 1 : 0);  // buffer stride in elements (bank skew)
+  static constexpr size_t off_buf = 0;
+  static constexpr size_t off_stage = ((size_t)KI * BUFS * D + 15) / 16 * 16;
+  static constexpr size_t off_tree = off_stage + (size_t)T * D;
+  static constexpr size_t off_u32 = off_tree + 2 * KI * sizeof(Key);
+  // u32 arrays: tcnt, cnt, plan (KI each), ws (32); then the block -> (bucket, index) map
+  static constexpr size_t off_blkb = off_u32 + (3 * KI + 32) * 4;
+  static constexpr int MAXBLK = T / B + KI;
+  static constexpr int LUT_BITS = 13;
+  static constexpr size_t off_lut = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
+  static constexpr size_t bytes = off_lut + ((size_t)4 << LUT_BITS);
+};
+
+template <int DT, int ALGO>
+__global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  using Unit = typename Tr::Unit;  // one element
+  using S = ClsV2<DT>;
+  constexpr int NT = S::NT, T = S::T, IPT = S::IPT, B = Tr::B, KI = Tr::KIDX, BUFS = S::BUFS;
+  constexpr int NWARPS = NT / 32;
+  constexpr u32 NONE = 0xFFFFFFFFu;
+  static_assert(Tr::D == sizeof(Unit), "one unit per element");
+  static_assert(KI % 32 == 0 && KI <= NT && B <= 255, "plan packing");
+
+  extern __shared__ __align__(16) char smem[];
+  Unit *s_buf = reinterpret_cast<Unit *>(smem + S::off_buf);
+  Unit *s_stage = reinterpret_cast<Unit *>(smem + S::off_stage);
+  Key *s_tree = reinterpret_cast<Key *>(smem + S::off_tree);
+  Key *s_spl = s_tree + KI;
+  u32 *s_tcnt = reinterpret_cast<u32 *>(smem + S::off_u32);
+  u32 *s_cnt = s_tcnt + KI;
+  u32 *s_plan = s_cnt + KI;
+  u32 *s_ws = s_plan + KI;
+  unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
+  u32 *s_lut = reinterpret_cast<u32 *>(smem + S::off_lut);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u32 stripe = blockIdx.x;
+  const u32 ti = A.stripe_task[stripe];
+  const LevelTask &L = A.tasks[ti];
+  const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
+  const u32 dmask = L.K - 1;
+  const u64 size = L.t.size;
+  const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
+  const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
+  Unit *gtask = reinterpret_cast<Unit *>(A.base + L.t.begin * (u64)Tr::D);
+
+  if (ALGO == ALGO_TREE) {
+    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
+    for (int i = tid; i < (1 << l); i += NT) {
+      s_tree[i] = gt[i];
+      s_spl[i] = gt[KI + i];
+    }
+  }
+  for (int j = tid; j < KI; j += NT) {
+    s_tcnt[j] = 0;
+    s_cnt[j] = 0;
+  }
+  u32 myfill = 0;  // tid < KI: elements buffered for bucket tid
+
+  // Lookup table of starting leaves (see classify_reg_kernel): slot q covers
+  // [llo + q*2^ls, llo + (q+1)*2^ls) and stores a = #{splitters < its first
+  // key} and the number of splitters inside it (inclusive of its last key).
+  const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
+  Key llo = tlo, lhi = thi;
+  if (ALGO == ALGO_TREE) {
+    llo = key_from_words<Key>(L.lut_lo);
+    lhi = key_from_words<Key>(L.lut_hi);
+    if (llo < tlo) llo = tlo;
+    if (lhi > thi) lhi = thi;
+    if (lhi < llo) lhi = llo;
+  }
+  int ls = bitlen((Key)(lhi - llo)) - S::LUT_BITS;
+  if (ls < 0) ls = 0;
+  const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
+  const int nspl = (1 << l) - 1;
+  if (ALGO == ALGO_TREE) {
+    __syncthreads();
+    auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
+      u32 a = 0, b = (u32)nspl;
+      while (a < b) {
+        u32 mid = (a + b) >> 1;
+        if (s_spl[mid] < v) a = mid + 1;
+        else b = mid;
+      }
+      return a;
+    };
+    for (u32 q = tid; q < (1u << S::LUT_BITS); q += NT) {
+      u32 e = 0;
+      if (q < nlut_used) {
+        const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
+        const Key r1 = q + 1 == nlut_used ? thi : llo + (((Key)(q + 1)) << ls) - 1;
+        // a = #{splitters < r0}; the count covers splitters in [r0, r1] (a
+        // slot with none cannot hold a key equal to a splitter)
+        const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
+        e = a | ((b - a) << 16);
+      }
+      s_lut[q] = e;
+    }
+  }
+  const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
+  Key kmin = key_max<Key>(), kmax = (Key)0;
+
+  const u64 n = s1 > s0 ? s1 - s0 : 0;
+  const u64 ntiles = (n + T - 1) / T;
+  u64 front = 0;
+  Unit x[IPT], y[IPT], xl[IPT];
+  u32 sl[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    sl[k] = NONE;
+    const u64 i = s0 + tid + (u64)k * NT;
+    if (i < s1) x[k] = gtask[i];
+  }
+  __syncthreads();
+
+  for (u64 t = 0; t < ntiles; ++t) {
+    const u64 e0 = s0 + t * T;
+    const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
+    if (t + 2 < ntiles) {
+      const u64 p0 = e0 + 2 * (u64)T;
+      const u64 p1 = p0 + T < s1 ? p0 + T : s1;
+      prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), tid, 2);
+    }
+    if (t + 1 < ntiles) {
+      if (cnt == T && e0 + 2 * (u64)T <= s1) {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) y[k] = gtask[e0 + T + tid + (u64)k * NT];
+      } else {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          const u64 i = e0 + T + tid + (u64)k * NT;
+          if (i < s1) y[k] = gtask[i];
+        }
+      }
+    }
+    // ---- classify + rank (Alg. 1 batched over IPT elements; LUT start)
+    u32 bkt[IPT], rank[IPT];
+    {
+      Key key[IPT];
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
+      if (want_minmax) {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          if (tid + k * NT < cnt) {
+            kmin = key[k] < kmin ? key[k] : kmin;
+            kmax = key[k] > kmax ? key[k] : kmax;
+          }
+        }
+      }
+      if (ALGO == ALGO_TREE) {
+        u32 ent[IPT];
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          const Key dk = key[k] - llo;
+          u32 q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
+          ent[k] = s_lut[q];
+        }
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          u32 a = ent[k] & 0xFFFFu;
+          const u32 c = ent[k] >> 16;
+          if (c) {  // the slot holds splitters: lower bound among them
+            u32 b = a + c;
+            while (a < b) {
+              const u32 mid = (a + b) >> 1;
+              if (s_spl[mid] < key[k]) a = mid + 1;
+              else b = mid;
+            }
+            bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
+          } else {  // no splitter in the slot: no key here equals one, so
+                    // key < s_a, except above the last splitter (bucket 2s+1)
+            bkt[k] = eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+      }
+    }
+    if (cnt == T) {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) rank[k] = atomicAdd(&s_tcnt[bkt[k]], 1u);
+    } else {
+#pragma unroll
+      for (int k = 0; k < IPT; ++k) rank[k] = (tid + k * NT < cnt) ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;
+    }
+    __syncthreads();  // A: ranks final; the previous tile's blocks have been copied out
+
+    // ---- the previous tile's leftovers enter their buffers
+#pragma unroll
+    for (int k = 0; k < IPT; ++k)
+      if (sl[k] != NONE) s_buf[sl[k]] = xl[k];
+
+    // ---- plan: nb blocks per bucket; scan of (nb | staged blocks << 16)
+    u32 nb = 0, boff = 0, soff = 0;
+    if (tid < KI) {
+      const u32 tc = s_tcnt[tid];
+      s_tcnt[tid] = 0;
+      s_cnt[tid] += tc;
+      const u32 tot = myfill + tc;
+      nb = tot / B;
+      const u32 pv = nb | ((nb ? nb - 1 : 0u) << 16);
+      u32 incl = pv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 yv = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += yv;
+      }
+      if (lane == 31) s_ws[wid] = incl;
+      asm volatile("bar.sync 1, %0;" ::"n"(KI) : "memory");
+      const u32 wv = lane < KI / 32 ? s_ws[lane] : 0u;
+      const u32 wpre = __reduce_add_sync(0xffffffffu, lane < wid ? wv : 0u);
+      const u32 pre = wpre + incl - pv;
+      boff = pre & 0xFFFFu;
+      soff = pre >> 16;
+      s_plan[tid] = myfill | (nb << 8) | (soff << 16);
+      for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
+      if (tid == KI - 1) s_ws[KI / 32] = pre + pv;  // totals
+      myfill = tot - nb * B;
+    }
+    __syncthreads();  // B: plan visible
+    const u32 nblocks = s_ws[KI / 32] & 0xFFFFu;
+
+    // ---- scatter: buffer j, a staged block, or a leftover
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      sl[k] = NONE;
+      if (cnt == T || tid + k * NT < cnt) {
+        const u32 j = bkt[k];
+        const u32 pl = s_plan[j];
+        const u32 v = (pl & 0xFFu) + rank[k];
+        const u32 nbj = (pl >> 8) & 0xFFu;
+        if (v < (u32)B) {
+          s_buf[j * BUFS + v] = x[k];
+        } else if (v < nbj * B) {
+          s_stage[((pl >> 16) + v / B - 1) * B + (v % B)] = x[k];
+        } else {
+          sl[k] = j * BUFS + (v - nbj * B);
+          xl[k] = x[k];
+        }
+      }
+    }
+    __syncthreads();  // C: blocks complete
+
+    // ---- copy the emitted blocks to the stripe's write front; bucket j's
+    //      blocks are [boff_j, boff_j + nb_j): block 0 from buffer j, the
+    //      rest from the stage.  One warp per block.
+    {
+      const u32 half = (u32)lane >> 4, hl = (u32)lane & 15u;
+      for (u32 g = 2 * wid + half; g < nblocks; g += 2 * NWARPS) {  // a block per half-warp
+        const u32 jq = s_blkb[g];
+        const u32 j = jq & 0x1FFu, q = jq >> 9;
+        const Unit *src = q == 0 ? s_buf + j * BUFS : s_stage + ((s_plan[j] >> 16) + q - 1) * B;
+        Unit *dst = gtask + s0 + (front + g) * B;
+#pragma unroll
+        for (int e = 0; e < B / 16; ++e) dst[hl + 16 * e] = src[hl + 16 * e];
+      }
+    }
+    front += nblocks;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) x[k] = y[k];
+  }
+  __syncthreads();  // the last copies have read the buffers
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    if (sl[k] != NONE) s_buf[sl[k]] = xl[k];
+  __syncthreads();
+
+  // ---- outputs: counts, partial fill, full blocks, partial buffers
+  const u64 sbase = L.sbk_off + (u64)(stripe - L.stripe_first) * L.kidx;
+  if (tid < KI) s_plan[tid] = myfill;
+  __syncthreads();
+  for (int j = tid; j < (int)L.kidx; j += NT) {
+    A.counts[sbase + j] = s_cnt[j];
+    A.pfill[sbase + j] = s_plan[j];
+  }
+  if (tid == 0) A.fullblocks[stripe] = (u32)front;
+  for (int j = wid; j < K; j += NWARPS) {
+    const int f = (int)s_plan[j];
+    Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * Tr::D);
+    for (int u = lane; u < f; u += 32) dst[u] = s_buf[j * BUFS + u];
+  }
+  if constexpr (sizeof(Key) == 8) {
+    if (want_minmax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Key a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+      }
+      if (lane == 0) {
+        atomicMin(reinterpret_cast<unsigned long long *>(&A.minmax[0]), (unsigned long long)kmin);
+        atomicMax(reinterpret_cast<unsigned long long *>(&A.minmax[1]), (unsigned long long)kmax);
+      }
+    }
+  }
+}
+
+}  // namespace ips4o

@@ -167,6 +167,38 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
 // byte with acquire loads.  Same guarantee, no shared counters, no fences
 // (DESIGN "Permutation on the GPU").
 constexpr int PERM_WARPS = 8;
+#ifndef IPS4O_PERM_DIGIT_PACE_NS
+#define IPS4O_PERM_DIGIT_PACE_NS 100
+#endif
+constexpr int PERM_DIGIT_PACE_NS = IPS4O_PERM_DIGIT_PACE_NS;
+
+#ifdef IPS4O_PERM_CLOCKS
+// debug: per-warp cycles spent in fetch (incl. misses), swap atomics, swap
+// loads, empty-write waits, and number of swap steps
+__device__ unsigned long long g_perm_clk[6];
+#define PCLK_DECL long long pc_t0_ = 0, pc_acc_[6] = {0, 0, 0, 0, 0, 0};
+#define PCLK_START() pc_t0_ = clock64()
+#define PCLK_ADD(i) pc_acc_[i] += clock64() - pc_t0_
+#define PCLK_CNT(i) pc_acc_[i] += 1
+#define PCLK_FLUSH() \
+  if (lane == 0)     \
+    for (int q_ = 0; q_ < 6; ++q_) atomicAdd(&g_perm_clk[q_], (unsigned long long)pc_acc_[q_]);
+#else
+#define PCLK_DECL
+#define PCLK_START()
+#define PCLK_ADD(i)
+#define PCLK_CNT(i)
+#define PCLK_FLUSH()
+#endif
+
+#ifdef IPS4O_PERM_STATS
+// debug counters: fetch attempts, fetches, misses, swaps, skips, empty writes,
+// waits (empty writes that polled rdone), poll iterations
+__device__ unsigned long long g_perm_stats[8];
+#define PSTAT(i, v) atomicAdd(&g_perm_stats[i], (unsigned long long)(v))
+#else
+#define PSTAT(i, v)
+#endif
 constexpr int PERM_THREADS = PERM_WARPS * 32;
 
 __device__ __forceinline__ void st_release_u8(unsigned char *p, unsigned v) {
@@ -175,6 +207,23 @@ __device__ __forceinline__ void st_release_u8(unsigned char *p, unsigned v) {
 __device__ __forceinline__ unsigned ld_acquire_u8(const unsigned char *p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u8 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class Unit> __device__ __forceinline__ Unit ld_cg_unit(const Unit *p);
+template <> __device__ __forceinline__ u64 ld_cg_unit<u64>(const u64 *p) {
+  u64 v;
+  asm volatile("ld.global.cg.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+template <> __device__ __forceinline__ u32 ld_cg_unit<u32>(const u32 *p) {
+  u32 v;
+  asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+template <> __device__ __forceinline__ uint4 ld_cg_unit<uint4>(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
 
@@ -221,12 +270,14 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   auto blk_ptr = [&](u64 x) -> Unit * {
     return reinterpret_cast<Unit *>(x == pblk ? ovf : gtask + x * (u64)B * D);
   };
+  // all loads of a block are issued back to back (volatile: the compiler may
+  // not sink the later ones past the bucket test that only needs the first)
   auto load_blk = [&](u64 x, Unit(&r)[NPL]) {
     const Unit *s = blk_ptr(x);
 #pragma unroll
     for (int i = 0; i < NPL; ++i) {
       int u = lane + 32 * i;
-      if (u < NU) r[i] = s[u];
+      if (u < NU) r[i] = ld_cg_unit(s + u);
     }
   };
   auto store_blk = [&](u64 x, const Unit(&r)[NPL]) {
@@ -251,21 +302,30 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
     if (lane == 0) {
       Key k = Tr::key(reinterpret_cast<const char *>(ku));
       b = ALGO == ALGO_TREE ? tree_bucket<Key>(s_tree, s_spl, l, eq, k) : digit_of(k, shift, dmask);
+      // Pacing: with the one-instruction digit, agents return to the hot
+      // (w, r) words so fast that same-address atomics queue up at L2 and
+      // every step slows ~10x (measured: 7100-cycle atomics, 7600-cycle
+      // loads per step vs ~650/2400 with a ~100 ns gap; the tree walk
+      // provides that gap by itself).
+      if (ALGO == ALGO_DIGIT) __nanosleep(PERM_DIGIT_PACE_NS);
     }
     return __shfl_sync(0xffffffffu, b, 0);
   };
 
   Unit buf0[NPL], buf1[NPL];
   int misses = 0;  // consecutive primary buckets without unprocessed blocks
+  PCLK_DECL
   for (;;) {
     // ---- fetch an unprocessed block from the primary bucket
     u64 x = ~0ull;
+    PCLK_START();
     while (misses < K) {
       u64 got = 0;
       if (lane == 0) {
         u64 cur = ld_relaxed_u64(&wr[(u64)p * WR_STRIDE]);
         i64 w = (i64)(cur >> 32), r = (i64)(cur & 0xFFFFFFFFull) - (i64)RBIAS;
         if (r >= w) {
+          PSTAT(0, 1);
           u64 old = atomicAdd(&wr[(u64)p * WR_STRIDE], ~0ull);  // r -= 1
           w = (i64)(old >> 32);
           r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
@@ -275,13 +335,16 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
       got = __shfl_sync(0xffffffffu, got, 0);
       if (got) {
         x = got & ~(1ull << 63);
+        if (lane == 0) PSTAT(1, 1);
         break;
       }
+      if (lane == 0) PSTAT(2, 1);
       p = p + 1 == K ? 0 : p + 1;
       ++misses;
     }
     if (x == ~0ull) break;  // a whole cycle without work: done
     misses = 0;
+    PCLK_ADD(0);
     load_blk(x, buf0);
     {
       // every lane's loads have returned once the reduction has its operands;
@@ -297,14 +360,23 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
     // ---- place buf0 into dest, swapping while dest has unprocessed blocks
     for (;;) {
       u64 old = 0;
+      PCLK_START();
       if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
       old = __shfl_sync(0xffffffffu, old, 0);
+      PCLK_ADD(1);
+      PCLK_CNT(4);
       const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
       if (w <= r) {
         // unprocessed block at w: swap, or skip it if already in place
+        PCLK_START();
         load_blk((u64)w, buf1);
         const u32 b2 = bucket_of(buf1);
-        if (b2 == dest) continue;
+        PCLK_ADD(2);
+        if (b2 == dest) {
+          if (lane == 0) PSTAT(4, 1);
+          continue;
+        }
+        if (lane == 0) PSTAT(3, 1);
         store_blk((u64)w, buf0);
 #pragma unroll
         for (int i = 0; i < NPL; ++i) buf0[i] = buf1[i];
@@ -313,18 +385,26 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
       }
       // empty block at w.  If it was full before the permutation, its
       // reader must be done.
+      PCLK_START();
       if (lane == 0) {
         const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
+        PSTAT(5, 1);
         if ((u64)w < pe) {
-          while (ld_acquire_u8(rdone + w) == 0) __nanosleep(32);
+          PSTAT(6, 1);
+          while (ld_acquire_u8(rdone + w) == 0) {
+            PSTAT(7, 1);
+            __nanosleep(32);
+          }
         }
         if ((u64)w == pblk) A.ovf_used[ti] = dest;
       }
       __syncwarp();
+      PCLK_ADD(3);
       store_blk((u64)w, buf0);
       break;
     }
   }
+  PCLK_FLUSH()
 }
 
 }  // namespace ips4o

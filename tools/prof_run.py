@@ -17,6 +17,8 @@ def main():
     ap.add_argument("--algo", default="tree")
     ap.add_argument("--base-cap", type=int, default=0)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--max-levels", type=int, default=0)
+    ap.add_argument("--nexact", type=int, default=0, help="element count (overrides --n)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -25,13 +27,13 @@ def main():
     import synth_inputs as gen
 
     dt = {"pairs": 2, "records100": 3}.get(a.dist, 1 if a.dist.endswith("_f64") else 0)
-    host = np.ascontiguousarray(gen.generate(a.dist, 1 << a.n, 42)).view(np.uint8).reshape(-1)
+    host = np.ascontiguousarray(gen.generate(a.dist, a.nexact or (1 << a.n), 42)).view(np.uint8).reshape(-1)
     src = torch.from_numpy(host).cuda()
     work = torch.empty_like(src)
     algo = ips.DIGIT if a.algo == "digit" else ips.TREE
     for r in range(a.reps):
         work.copy_(src)
-        st = ips.sort_ex(work, dt, algo=algo, base_cap=a.base_cap, timing=True)
+        st = ips.sort_ex(work, dt, algo=algo, base_cap=a.base_cap, timing=True, max_levels=a.max_levels)
         torch.cuda.synchronize()
         print(r, {k: round(v, 3) for k, v in st["kernel_ms"].items() if v}, st["levels"], st["tasks_per_level"])
     if a.check and dt == 0:
