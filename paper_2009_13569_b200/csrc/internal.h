@@ -85,6 +85,7 @@ struct LevelArgs {
   char *overflow;             // [ntasks][b*D] overflow blocks
   u32 *ovf_used;              // [ntasks] bucket that wrote the overflow block, or ~0
   unsigned char *rdone;       // [blk_off + x] block x of the task has been read (K4)
+  u32 *task_done;             // [ntasks] no block of the task can be fetched any more (K4)
   // scheduler outputs
   TaskDesc *next_tasks;       // next level
   TaskDesc *base_tasks;       // base-case tasks of this level

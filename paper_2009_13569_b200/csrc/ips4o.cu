@@ -177,6 +177,7 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.overflow = ar.take<char>(T * (size_t)B * D);
   A.ovf_used = ar.take<u32>(T);
   A.rdone = ar.take<unsigned char>(P.nblk);
+  A.task_done = ar.take<u32>(T);
   A.minmax = ar.take<u64>(2);
   A.next_tasks = ar.take<TaskDesc>(P.child_cap);
   A.base_tasks = ar.take<TaskDesc>(P.child_cap);
@@ -359,6 +360,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CK(cudaMemcpyAsync((void *)A.perm_task, hp + T * sizeof(LevelTask) + S * 4, NP * 4, cudaMemcpyHostToDevice, c.st));
   CK(cudaMemsetAsync(A.counters, 0, 16 * 4, c.st));
   CK(cudaMemsetAsync(A.rdone, 0, P.nblk, c.st));
+  CK(cudaMemsetAsync(A.task_done, 0, T * 4, c.st));
   CK(cudaMemsetAsync(A.minmax, 0xFF, 8, c.st));  // min = all ones
   CK(cudaMemsetAsync(A.minmax + 1, 0, 8, c.st));  // max = 0
   c.ms[KF_HOST] += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();

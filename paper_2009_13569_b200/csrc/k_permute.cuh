@@ -232,6 +232,18 @@ template <> __device__ __forceinline__ u32 fold32<u64>(const u64 &u) { return (u
 template <> __device__ __forceinline__ u32 fold32<u32>(const u32 &u) { return u; }
 template <> __device__ __forceinline__ u32 fold32<uint4>(const uint4 &u) { return u.x ^ u.y ^ u.z ^ u.w; }
 
+__device__ __forceinline__ u32 ld_relaxed_u32(const u32 *p) {
+  u32 v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Agents (warps) start on the task of their CTA (agents per task in
+// proportion to its size) and, once no block of it can be fetched
+// any more, move on to the next unfinished task of the level, so that the
+// level ends when the last block is placed rather than when the slowest task's
+// own agents are done.  The protocol per task is unchanged; it does not care
+// which agents take part.
 template <int DT, int ALGO>
 __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
@@ -242,167 +254,207 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   constexpr int NPL = (NU + 31) / 32;
   __shared__ Key s_tree[KI], s_spl[KI];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const u32 cta = blockIdx.x;
-  const u32 ti = A.perm_task[cta];
-  const LevelTask &L = A.tasks[ti];
-  const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
-  const u32 dmask = L.K - 1;
+  const u32 home = A.perm_task[blockIdx.x];
   if (ALGO == ALGO_TREE) {
-    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
-    for (int i = threadIdx.x; i < (1 << l); i += PERM_THREADS) {
+    const LevelTask &H = A.tasks[home];
+    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)home * 2 * KI;
+    for (int i = threadIdx.x; i < (1 << H.l); i += PERM_THREADS) {
       s_tree[i] = gt[i];
       s_spl[i] = gt[KI + i];
     }
   }
   __syncthreads();
-  if (K <= 1) return;
   if (A.dbg_one_agent && wid != 0) return;
-  char *gtask = A.base + L.t.begin * (u64)D;
-  const u64 size = L.t.size;
-  const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow
-  char *ovf = A.overflow + (size_t)ti * B * D;
-  u64 *wr = A.wr + L.bucket_off * WR_STRIDE;
-  unsigned char *rdone = A.rdone + L.blk_off;
-  const u32 agent = (cta - L.perm_first) * PERM_WARPS + wid;
-  const u32 nagents = A.dbg_one_agent ? 1 : L.nperm * PERM_WARPS;
-  int p = (int)(((u64)agent * (u64)K) / nagents);  // P:847 starting points spread
-
-  auto blk_ptr = [&](u64 x) -> Unit * {
-    return reinterpret_cast<Unit *>(x == pblk ? ovf : gtask + x * (u64)B * D);
-  };
-  // all loads of a block are issued back to back (volatile: the compiler may
-  // not sink the later ones past the bucket test that only needs the first)
-  auto load_blk = [&](u64 x, Unit(&r)[NPL]) {
-    const Unit *s = blk_ptr(x);
-#pragma unroll
-    for (int i = 0; i < NPL; ++i) {
-      int u = lane + 32 * i;
-      if (u < NU) r[i] = ld_cg_unit(s + u);
-    }
-  };
-  auto store_blk = [&](u64 x, const Unit(&r)[NPL]) {
-    Unit *d = blk_ptr(x);
-#pragma unroll
-    for (int i = 0; i < NPL; ++i) {
-      int u = lane + 32 * i;
-      if (u < NU) d[u] = r[i];
-    }
-  };
-  // bucket of the block held in registers: its key is in the first KEY_UNITS
-  // units, i.e. on lanes 0..KEY_UNITS-1 of register 0
-  auto bucket_of = [&](const Unit(&r)[NPL]) -> u32 {
-    Unit ku[Tr::KEY_UNITS];
-    if constexpr (Tr::KEY_UNITS == 1) {
-      ku[0] = r[0];
-    } else {
-#pragma unroll
-      for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = __shfl_sync(0xffffffffu, r[0], q);
-    }
-    u32 b = 0;
-    if (lane == 0) {
-      Key k = Tr::key(reinterpret_cast<const char *>(ku));
-      b = ALGO == ALGO_TREE ? tree_bucket<Key>(s_tree, s_spl, l, eq, k) : digit_of(k, shift, dmask);
-      // Pacing: with the one-instruction digit, agents return to the hot
-      // (w, r) words so fast that same-address atomics queue up at L2 and
-      // every step slows ~10x (measured: 7100-cycle atomics, 7600-cycle
-      // loads per step vs ~650/2400 with a ~100 ns gap; the tree walk
-      // provides that gap by itself).
-      if (ALGO == ALGO_DIGIT) __nanosleep(PERM_DIGIT_PACE_NS);
-    }
-    return __shfl_sync(0xffffffffu, b, 0);
-  };
-
-  Unit buf0[NPL], buf1[NPL];
-  int misses = 0;  // consecutive primary buckets without unprocessed blocks
+  const u32 agent = (blockIdx.x - A.tasks[home].perm_first) * PERM_WARPS + wid;
   PCLK_DECL
-  for (;;) {
-    // ---- fetch an unprocessed block from the primary bucket
-    u64 x = ~0ull;
-    PCLK_START();
-    while (misses < K) {
-      u64 got = 0;
-      if (lane == 0) {
-        u64 cur = ld_relaxed_u64(&wr[(u64)p * WR_STRIDE]);
-        i64 w = (i64)(cur >> 32), r = (i64)(cur & 0xFFFFFFFFull) - (i64)RBIAS;
-        if (r >= w) {
-          PSTAT(0, 1);
-          u64 old = atomicAdd(&wr[(u64)p * WR_STRIDE], ~0ull);  // r -= 1
-          w = (i64)(old >> 32);
-          r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
-          if (r >= w) got = 1ull << 63 | (u64)r;
-        }
+
+  u32 ti = home;
+  for (u32 hop = 0; hop < A.ntasks; ++hop) {
+    if (hop > 0) {
+      if (A.dbg_one_agent) break;
+      // next unfinished task after ti (32 done flags per probe)
+      u32 nxt = ~0u;
+      for (u32 base = 1; base < A.ntasks && nxt == ~0u; base += 32) {
+        u32 q = ti + base + lane;
+        q = q >= A.ntasks ? q - A.ntasks : q;
+        const bool open = base + lane < A.ntasks && ld_relaxed_u32(&A.task_done[q]) == 0;
+        const unsigned m = __ballot_sync(0xffffffffu, open);
+        if (m) nxt = __shfl_sync(0xffffffffu, q, __ffs(m) - 1);
       }
-      got = __shfl_sync(0xffffffffu, got, 0);
-      if (got) {
-        x = got & ~(1ull << 63);
-        if (lane == 0) PSTAT(1, 1);
-        break;
-      }
-      if (lane == 0) PSTAT(2, 1);
-      p = p + 1 == K ? 0 : p + 1;
-      ++misses;
+      if (nxt == ~0u) break;
+      hop += (nxt >= ti ? nxt - ti : nxt + A.ntasks - ti) - 1;
+      ti = nxt;
     }
-    if (x == ~0ull) break;  // a whole cycle without work: done
-    misses = 0;
-    PCLK_ADD(0);
-    load_blk(x, buf0);
-    {
-      // every lane's loads have returned once the reduction has its operands;
-      // then publish "block x read" (release) for a writer waiting on it
-      u32 v = 0;
+    const LevelTask &L = A.tasks[ti];
+    const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
+    if (K <= 1) {
+      if (lane == 0) atomicExch(&A.task_done[ti], 1u);
+      continue;
+    }
+    const u32 dmask = L.K - 1;
+    const bool local = ti == home;
+    const Key *tr = local ? s_tree : reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
+    const Key *sp = local ? s_spl : tr + KI;
+    char *gtask = A.base + L.t.begin * (u64)D;
+    const u64 size = L.t.size;
+    const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow
+    char *ovf = A.overflow + (size_t)ti * B * D;
+    u64 *wr = A.wr + L.bucket_off * WR_STRIDE;
+    unsigned char *rdone = A.rdone + L.blk_off;
+    const u32 nagents = A.dbg_one_agent ? 1 : L.nperm * PERM_WARPS;
+    // P:847 starting points spread over the buckets
+    int p = local ? (int)(((u64)agent * (u64)K) / nagents) : (int)((agent * 97u + blockIdx.x) % (u32)K);
+
+    auto blk_ptr = [&](u64 x) -> Unit * {
+      return reinterpret_cast<Unit *>(x == pblk ? ovf : gtask + x * (u64)B * D);
+    };
+    // all loads of a block are issued back to back (volatile: the compiler
+    // may not sink the later ones past the bucket test that needs the first)
+    auto load_blk = [&](u64 x, Unit(&r)[NPL]) {
+      const Unit *src = blk_ptr(x);
 #pragma unroll
-      for (int i = 0; i < NPL; ++i) v ^= fold32<Unit>(buf0[i]);
-      v = __reduce_xor_sync(0xffffffffu, v);
-      asm volatile("" ::"r"(v));  // keep the dependency on every lane's loads
-      if (lane == 0) st_release_u8(rdone + x, 1u);
-    }
-    u32 dest = bucket_of(buf0);
-    // ---- place buf0 into dest, swapping while dest has unprocessed blocks
+      for (int i = 0; i < NPL; ++i) {
+        int u = lane + 32 * i;
+        if (u < NU) r[i] = ld_cg_unit(src + u);
+      }
+    };
+    auto store_blk = [&](u64 x, const Unit(&r)[NPL]) {
+      Unit *d = blk_ptr(x);
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) {
+        int u = lane + 32 * i;
+        if (u < NU) d[u] = r[i];
+      }
+    };
+    // bucket of the block held in registers: its key is in the first
+    // KEY_UNITS units, i.e. on lanes 0..KEY_UNITS-1 of register 0
+    auto bucket_of = [&](const Unit(&r)[NPL]) -> u32 {
+      Unit ku[Tr::KEY_UNITS];
+      if constexpr (Tr::KEY_UNITS == 1) {
+        ku[0] = r[0];
+      } else {
+#pragma unroll
+        for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = __shfl_sync(0xffffffffu, r[0], q);
+      }
+      u32 b = 0;
+      if (lane == 0) {
+        Key k = Tr::key(reinterpret_cast<const char *>(ku));
+        b = ALGO == ALGO_TREE ? tree_bucket<Key>(tr, sp, l, eq, k) : digit_of(k, shift, dmask);
+        // Pacing: with the one-instruction digit, agents return to the hot
+        // (w, r) words so fast that same-address atomics queue up at L2 and
+        // every step slows ~10x (measured: 7100-cycle atomics, 7600-cycle
+        // loads per step vs ~650/2400 with a ~100 ns gap; the tree walk
+        // provides that gap by itself).
+        if (ALGO == ALGO_DIGIT) __nanosleep(PERM_DIGIT_PACE_NS);
+      }
+      return __shfl_sync(0xffffffffu, b, 0);
+    };
+
+    Unit buf0[NPL], buf1[NPL];
     for (;;) {
-      u64 old = 0;
+      // ---- fetch an unprocessed block: the primary bucket p
+      //      first; when it has none, the 32 lanes probe 32 buckets at a time
+      u64 x = ~0ull;
       PCLK_START();
-      if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
-      old = __shfl_sync(0xffffffffu, old, 0);
-      PCLK_ADD(1);
-      PCLK_CNT(4);
-      const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
-      if (w <= r) {
-        // unprocessed block at w: swap, or skip it if already in place
-        PCLK_START();
-        load_blk((u64)w, buf1);
-        const u32 b2 = bucket_of(buf1);
-        PCLK_ADD(2);
-        if (b2 == dest) {
-          if (lane == 0) PSTAT(4, 1);
-          continue;
-        }
-        if (lane == 0) PSTAT(3, 1);
-        store_blk((u64)w, buf0);
-#pragma unroll
-        for (int i = 0; i < NPL; ++i) buf0[i] = buf1[i];
-        dest = b2;
-        continue;
-      }
-      // empty block at w.  If it was full before the permutation, its
-      // reader must be done.
-      PCLK_START();
-      if (lane == 0) {
-        const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
-        PSTAT(5, 1);
-        if ((u64)w < pe) {
-          PSTAT(6, 1);
-          while (ld_acquire_u8(rdone + w) == 0) {
-            PSTAT(7, 1);
-            __nanosleep(32);
+      for (;;) {
+        u64 got = 0;
+        if (lane == 0) {
+          u64 cur = ld_relaxed_u64(&wr[(u64)p * WR_STRIDE]);
+          i64 w = (i64)(cur >> 32), r = (i64)(cur & 0xFFFFFFFFull) - (i64)RBIAS;
+          if (r >= w) {
+            PSTAT(0, 1);
+            u64 old = atomicAdd(&wr[(u64)p * WR_STRIDE], ~0ull);  // r -= 1
+            w = (i64)(old >> 32);
+            r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
+            if (r >= w) got = 1ull << 63 | (u64)r;
           }
         }
-        if ((u64)w == pblk) A.ovf_used[ti] = dest;
+        got = __shfl_sync(0xffffffffu, got, 0);
+        if (got) {
+          x = got & ~(1ull << 63);
+          if (lane == 0) PSTAT(1, 1);
+          break;
+        }
+        if (lane == 0) PSTAT(2, 1);
+        // r and w only move towards each other: a bucket seen without work
+        // stays without work, so one sweep without any means the task is done
+        int found = -1;
+        for (int base = 0; base < K && found < 0; base += 32) {
+          int q = p + base + lane;
+          q = q >= K ? q - K : q;
+          bool has = false;
+          if (base + lane < K) {
+            const u64 cur = ld_relaxed_u64(&wr[(u64)q * WR_STRIDE]);
+            has = (i64)(cur & 0xFFFFFFFFull) - (i64)RBIAS >= (i64)(cur >> 32);
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, has);
+          if (m) found = __shfl_sync(0xffffffffu, q, __ffs(m) - 1);
+        }
+        if (found < 0) break;
+        p = found;
       }
-      __syncwarp();
-      PCLK_ADD(3);
-      store_blk((u64)w, buf0);
-      break;
+      if (x == ~0ull) break;
+      PCLK_ADD(0);
+      load_blk(x, buf0);
+      {
+        // every lane's loads have returned once the reduction has its
+        // operands; then publish "block x read" (release) for a writer
+        u32 v = 0;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) v ^= fold32<Unit>(buf0[i]);
+        v = __reduce_xor_sync(0xffffffffu, v);
+        asm volatile("" ::"r"(v));  // keep the dependency on every lane's loads
+        if (lane == 0) st_release_u8(rdone + x, 1u);
+      }
+      u32 dest = bucket_of(buf0);
+      // ---- place buf0 into dest, swapping while dest has unprocessed blocks
+      for (;;) {
+        u64 old = 0;
+        PCLK_START();
+        if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
+        old = __shfl_sync(0xffffffffu, old, 0);
+        PCLK_ADD(1);
+        PCLK_CNT(4);
+        const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
+        if (w <= r) {
+          // unprocessed block at w: swap, or skip it if already in place
+          PCLK_START();
+          load_blk((u64)w, buf1);
+          const u32 b2 = bucket_of(buf1);
+          PCLK_ADD(2);
+          if (b2 == dest) {
+            if (lane == 0) PSTAT(4, 1);
+            continue;
+          }
+          if (lane == 0) PSTAT(3, 1);
+          store_blk((u64)w, buf0);
+#pragma unroll
+          for (int i = 0; i < NPL; ++i) buf0[i] = buf1[i];
+          dest = b2;
+          continue;
+        }
+        // empty block at w.  If it was full before the permutation,
+        // its reader must be done.
+        PCLK_START();
+        if (lane == 0) {
+          const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
+          PSTAT(5, 1);
+          if ((u64)w < pe) {
+            PSTAT(6, 1);
+            while (ld_acquire_u8(rdone + w) == 0) {
+              PSTAT(7, 1);
+              __nanosleep(32);
+            }
+          }
+          if ((u64)w == pblk) A.ovf_used[ti] = dest;
+        }
+        __syncwarp();
+        PCLK_ADD(3);
+        store_blk((u64)w, buf0);
+        break;
+      }
     }
+    if (lane == 0) atomicExch(&A.task_done[ti], 1u);
   }
   PCLK_FLUSH()
 }
