@@ -131,7 +131,6 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
   __shared__ u32 s_nbig;
-  __shared__ u64 s_mul;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
@@ -154,25 +153,24 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
     const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
     if (m <= 1 || !(lo < hi)) continue;
-    // digit(x) = floor(((x - lo) >> ds) * dmul / 2^64): monotone in x and
-    // spread evenly over nd digits, ~1 element per digit (nd = pow2 >= m).
-    // Key ranges narrower than nd use the offset itself (one key per digit).
+    // digit(x) = floor(v(x) * dmul / 2^32) with v(x) = the top 32 bits of
+    // x - lo over the bucket's range: monotone in x (all the counting sort
+    // needs; the runs are finished by key comparisons) and spread evenly over
+    // nd digits, ~1 element per digit (nd = pow2 >= m).  Ranges narrower than
+    // nd use v itself (one key per digit when ds == 0).
     int lg = 1;
     while ((1 << lg) < m && lg < BI::DBMAX) ++lg;
     const Key range = hi - lo;
     const int bits = bitlen(range);
-    const int ds = bits > 64 ? bits - 64 : 0;
-    const u64 r64 = (u64)(range >> ds);
-    const bool direct = r64 < (1ull << lg);
-    const int nd = direct ? (int)r64 + 1 : (1 << lg);
+    const int ds = bits > 32 ? bits - 32 : 0;
+    const u32 r32 = (u32)(range >> ds);
+    const bool direct = r32 < (1u << lg);
+    const int nd = direct ? (int)r32 + 1 : (1 << lg);
     const bool exact = direct && ds == 0;  // a digit holds a single key value
-    if (tid == 0) {
-      s_mul = direct ? 0ull
-                     : (r64 == ~0ull ? (1ull << lg) : (u64)(((u128)1 << (64 + lg)) / ((u128)r64 + 1)));
-    }
+    const u32 dmul = direct ? 1u : (u32)((1ull << (32 + lg)) / ((u64)r32 + 1));
     auto digit = [&](const Item &it) -> u32 {
-      const u64 v = (u64)((BI::key(it) - lo) >> ds);
-      return direct ? (u32)v : (u32)__umul64hi(v, s_mul);
+      const u32 v = (u32)((BI::key(it) - lo) >> ds);
+      return direct ? v : __umulhi(v, dmul);
     };
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
     for (int w = tid; w < nw; w += NT) s_hist[w] = 0;
