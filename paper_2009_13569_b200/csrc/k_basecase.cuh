@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       return direct ? v : __umulhi(v, dmul);
     };
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
-    for (int w = tid; w < nw; w += NT) s_hist[w] = 0;
+    for (int w = tid; w < (1 << BI::DBMAX) / 8; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
     if (tid == 0) s_nbig = 0;
     if constexpr (BI::STAGE_RECORDS) {
       // stage the records (coalesced u32 copy)
@@ -202,47 +202,56 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
     __syncthreads();
     BC_PHASE(1)
-    // 2. exclusive scan in place; warp w owns a contiguous chunk of words and
-    //    walks it 32 at a time.  Each word becomes (start(2w), start(2w+1)).
+    // 2. exclusive scan in place: thread t owns the WPT consecutive words
+    //    [t*WPT, (t+1)*WPT) (vector loads), one block-wide scan of the thread
+    //    totals.  Each word becomes (start(2w), start(2w+1)).
     {
-      constexpr int NW = NT / 32;
-      const int chunk = ((nw + NW - 1) / NW + 31) & ~31;
-      const int c0 = wid * chunk, c1 = c0 + chunk < nw ? c0 + chunk : nw;
-      u32 part = 0;
-      for (int w = c0 + lane; w < c1; w += 32) {
-        const u32 h = s_hist[w];
-        part += (h & 0xFFFFu) + (h >> 16);
-      }
-      part = __reduce_add_sync(0xffffffffu, part);
-      if (lane == 0) s_ws[wid] = part;
-      __syncthreads();
-      u32 off = __reduce_add_sync(0xffffffffu, lane < wid ? s_ws[lane] : 0u);
-      for (int w0 = c0; w0 < c1; w0 += 32) {
-        const int w = w0 + lane;
-        const u32 h = w < c1 ? s_hist[w] : 0u;
-        const u32 v = (h & 0xFFFFu) + (h >> 16);
-        u32 x = v;
+      constexpr int WPT = ((1 << BI::DBMAX) / 2 + NT - 1) / NT;
+      u32 h[WPT];
+      if constexpr (WPT % 4 == 0) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
+        for (int q = 0; q < WPT / 4; ++q) {
+          const uint4 v4 = reinterpret_cast<const uint4 *>(s_hist)[tid * (WPT / 4) + q];
+          h[4 * q] = v4.x;
+          h[4 * q + 1] = v4.y;
+          h[4 * q + 2] = v4.z;
+          h[4 * q + 3] = v4.w;
         }
-        const u32 st = off + x - v;
-        if (w < c1) {
-          s_hist[w] = st | ((st + (h & 0xFFFFu)) << 16);
-          // runs longer than RANKMAX are listed for the warp bitonic sort
-          if (!exact && v > RANKMAX) {
-            if ((h & 0xFFFFu) > RANKMAX) {
-              const u32 slot = atomicAdd(&s_nbig, 1u);
-              if (slot < BIGCAP) s_big[slot] = 2u * w;
-            }
-            if ((h >> 16) > RANKMAX) {
-              const u32 slot = atomicAdd(&s_nbig, 1u);
-              if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
-            }
+      } else {
+#pragma unroll
+        for (int q = 0; q < WPT; ++q) h[q] = s_hist[tid * WPT + q];
+      }
+      u32 tot = 0;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) tot += (h[q] & 0xFFFFu) + (h[q] >> 16);
+      u32 all;
+      u32 st = block_exclusive_scan<NT>(tot, s_ws, &all);
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        const u32 c0 = h[q] & 0xFFFFu, c1 = h[q] >> 16;
+        const u32 w = (u32)(tid * WPT + q);
+        // runs longer than RANKMAX are listed for the warp bitonic sort
+        if (!exact && (c0 > RANKMAX || c1 > RANKMAX) && w < (u32)nw) {
+          if (c0 > RANKMAX) {
+            const u32 slot = atomicAdd(&s_nbig, 1u);
+            if (slot < BIGCAP) s_big[slot] = 2u * w;
+          }
+          if (c1 > RANKMAX) {
+            const u32 slot = atomicAdd(&s_nbig, 1u);
+            if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
           }
         }
-        off += __shfl_sync(0xffffffffu, x, 31);
+        h[q] = st | ((st + c0) << 16);
+        st += c0 + c1;
+      }
+      if constexpr (WPT % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < WPT / 4; ++q)
+          reinterpret_cast<uint4 *>(s_hist)[tid * (WPT / 4) + q] =
+              make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < WPT; ++q) s_hist[tid * WPT + q] = h[q];
       }
     }
     __syncthreads();
