@@ -625,7 +625,8 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   constexpr int NWARPS = NT / 32;
   constexpr u32 NONE = 0xFFFFFFFFu;
   static_assert(Tr::D == sizeof(Unit), "one unit per element");
-  static_assert(KI % 32 == 0 && KI <= NT && B <= 255, "plan packing");
+  static_assert(KI % 32 == 0 && KI <= NT && B <= 255 && (T / B + 1) * B < 8192 && T / B < 2048, "plan packing");
+  constexpr u32 STG0 = (u32)(S::off_stage / sizeof(Unit));  // stage start, in elements from s_buf
 
   extern __shared__ __align__(16) char smem[];
   Unit *s_buf = reinterpret_cast<Unit *>(smem + S::off_buf);
@@ -722,10 +723,10 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   for (u64 t = 0; t < ntiles; ++t) {
     const u64 e0 = s0 + t * T;
     const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
-    if (t + 2 < ntiles) {
+    if (wid == 0 && t + 2 < ntiles) {
       const u64 p0 = e0 + 2 * (u64)T;
       const u64 p1 = p0 + T < s1 ? p0 + T : s1;
-      prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), tid, 2);
+      prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), lane, 2);
     }
     if (t + 1 < ntiles) {
       if (cnt == T && e0 + 2 * (u64)T <= s1) {
@@ -820,7 +821,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       const u32 pre = wpre + incl - pv;
       boff = pre & 0xFFFFu;
       soff = pre >> 16;
-      s_plan[tid] = myfill | (nb << 8) | (soff << 16);
+      s_plan[tid] = myfill | ((nb * B) << 8) | (soff << 21);
       for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
       if (tid == KI - 1) s_ws[KI / 32] = pre + pv;  // totals
       myfill = tot - nb * B;
@@ -828,24 +829,22 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     __syncthreads();  // B: plan visible
     const u32 nblocks = s_ws[KI / 32] & 0xFFFFu;
 
-    // ---- scatter: buffer j, a staged block, or a leftover
+    // ---- scatter: buffer j, a staged block, or a leftover.  The staged
+    //      runs of bucket j start at element STG0 + soff_j*B and element v
+    //      (v >= B) of the bucket's tile run lands at STG0 + soff_j*B + v - B:
+    //      one address formula, no per-element branches.
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      sl[k] = NONE;
-      if (cnt == T || tid + k * NT < cnt) {
-        const u32 j = bkt[k];
-        const u32 pl = s_plan[j];
-        const u32 v = (pl & 0xFFu) + rank[k];
-        const u32 nbj = (pl >> 8) & 0xFFu;
-        if (v < (u32)B) {
-          s_buf[j * BUFS + v] = x[k];
-        } else if (v < nbj * B) {
-          s_stage[((pl >> 16) + v / B - 1) * B + (v % B)] = x[k];
-        } else {
-          sl[k] = j * BUFS + (v - nbj * B);
-          xl[k] = x[k];
-        }
-      }
+      const bool valid = cnt == T || tid + k * NT < cnt;
+      const u32 j = valid ? bkt[k] : 0u;
+      const u32 pl = s_plan[j];
+      const u32 v = (pl & 0xFFu) + rank[k];
+      const u32 cut = (pl >> 8) & 0x1FFFu;
+      const u32 pos = v < (u32)B ? j * BUFS + v : STG0 + (pl >> 21) * B + v - B;
+      const bool keep = v < cut || v < (u32)B;
+      if (valid && keep) s_buf[pos] = x[k];
+      sl[k] = (valid && !keep) ? j * BUFS + (v - cut) : NONE;
+      xl[k] = x[k];
     }
     __syncthreads();  // C: blocks complete
 
@@ -857,7 +856,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       for (u32 g = 2 * wid + half; g < nblocks; g += 2 * NWARPS) {  // a block per half-warp
         const u32 jq = s_blkb[g];
         const u32 j = jq & 0x1FFu, q = jq >> 9;
-        const Unit *src = q == 0 ? s_buf + j * BUFS : s_stage + ((s_plan[j] >> 16) + q - 1) * B;
+        const Unit *src = q == 0 ? s_buf + j * BUFS : s_stage + ((s_plan[j] >> 21) + q - 1) * B;
         Unit *dst = gtask + s0 + (front + g) * B;
 #pragma unroll
         for (int e = 0; e < B / 16; ++e) dst[hl + 16 * e] = src[hl + 16 * e];
