@@ -74,6 +74,8 @@ struct LevelArgs {
   void *trees;                // [ntasks][2][KIDX] keys (tree | splitter)
   u32 *counts;                // [stripe-bucket slot] elements per bucket per stripe
   u32 *pfill;                 // [stripe-bucket slot] elements left in partial buffers
+  u32 *pcum;                  // [stripe-bucket slot] exclusive prefix over the task's stripes of pfill
+  u32 *ptot;                  // [bucket_off + j] partial-buffer elements of bucket j (all stripes)
   u32 *fullblocks;            // [nstripes] full blocks flushed per stripe
   u32 *fcum;                  // [nstripes] exclusive prefix of fullblocks within the task
   char *partials;             // [stripe-bucket slot][b*D] partial buffer contents

@@ -167,6 +167,8 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.trees = ar.take<Key>(T * 2 * KI);
   A.counts = ar.take<u32>(P.nsbk);
   A.pfill = ar.take<u32>(P.nsbk);
+  A.pcum = ar.take<u32>(P.nsbk);
+  A.ptot = ar.take<u32>(P.nbk);
   A.fullblocks = ar.take<u32>(S);
   A.fcum = ar.take<u32>(S);
   A.partials = ar.take<char>(P.nsbk * (size_t)B * D);
@@ -215,7 +217,6 @@ template <int DT, int ALGO> static int set_attrs() {
   CK(cudaFuncSetAttribute(sample_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sample_max<DT>() * sizeof(typename Traits<DT>::Key))));
   CK(cudaFuncSetAttribute(stripe_fix_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  CK(cudaFuncSetAttribute(cleanup_fill_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
   return 0;
 }
@@ -385,7 +386,6 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   boundaries_kernel<DT><<<(unsigned)T, BND_THREADS, 0, c.st>>>(A);
   CKLAUNCH();
   if ((rc = mark(c, KF_BOUND))) return rc;
-  const size_t cum_smem = ((size_t)P.max_stripes_per_task + 1) * 4;
   stripe_fix_kernel<DT><<<(unsigned)S, FIX_THREADS, 0, c.st>>>(A);
   CKLAUNCH();
   if ((rc = mark(c, KF_FIX))) return rc;
@@ -426,7 +426,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   // K5 cleanup
   cleanup_save_kernel<DT><<<dim3((KI + CLN_WARPS - 1) / CLN_WARPS, (unsigned)T), CLN_WARPS * 32, 0, c.st>>>(A);
   CKLAUNCH();
-  cleanup_fill_kernel<DT><<<dim3(KI, (unsigned)T), FILL_THREADS, cum_smem, c.st>>>(A);
+  cleanup_fill_kernel<DT><<<dim3(P.max_stripes_per_task, (unsigned)T), FILL_THREADS, 0, c.st>>>(A);
   CKLAUNCH();
   if ((rc = mark(c, KF_CLEAN))) return rc;
   const bool last_level = c.max_levels > 0 && level_no + 1 >= c.max_levels;

@@ -47,6 +47,15 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
       dst[u] = logical(o0 + e)[w];
     }
   }
+  if (lane == 0) {
+    // invariant of the cleanup: #holes = overlap + partial buffers (+ the
+    // overflow block, placed below); a violation is reported, never silent
+    const u64 hd = d0 < E1 ? d0 : E1;
+    const u64 tl = W > hd ? W : hd;
+    const u64 nholes = (hd - A.E[bo + j]) + (tl < E1 ? E1 - tl : 0);
+    const u64 o = W > o0 ? W - o0 : 0;
+    if (nholes != o + A.ptot[bo + j]) atomicAdd(&A.counters[4], 1u);
+  }
   if (ovb == (u32)j) {
     const u64 p0 = pblk * B;
     const u64 hi = E1 < size ? E1 : size;
@@ -58,11 +67,15 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
 }
 
 // ------------------------------------------------------------------ K5b
-// Phase b (one CTA per bucket): fill the holes of bucket j -- its head
-// [E_j, min(d_j, E_{j+1})) and its tail [w_j*b, E_{j+1}) -- with the saved
-// overlap of bucket j and the partial buffers of every stripe of the task
-// (the misplaced elements are in the head of b_{i+1}, in the
-// partially filled buffers, or in the overflow block).
+// Phase b: fill the holes of every bucket j -- its head [E_j, min(d_j,
+// E_{j+1})) and its tail [w_j*b, E_{j+1}) -- with the saved overlap of bucket
+// j and the partial buffers of every stripe of the task (the
+// misplaced elements are in the head of b_{i+1}, in the partially filled
+// buffers, or in the overflow block).  Hole h of bucket j (heads first) takes
+// overlap element h for h < o, then the partial buffers in stripe order:
+// stripe s's buffer fills holes [o + pcum_s, o + pcum_s + pfill_s).  One CTA
+// per (stripe, task), a warp per bucket, coalesced copies of each buffer;
+// the CTA of stripe 0 also places the overlaps.
 constexpr int FILL_THREADS = 256;
 
 template <int DT>
@@ -71,64 +84,40 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
   using Unit = typename Tr::Unit;
   constexpr int D = Tr::D, B = Tr::B;
   constexpr int UPE = D / (int)sizeof(Unit);
-  extern __shared__ __align__(16) u32 s_cum[];  // [nstripes + 1]
-  __shared__ u32 ws[FILL_THREADS / 32 + 1];
+  constexpr int NW = FILL_THREADS / 32;
   const u32 ti = blockIdx.y;
   const LevelTask &L = A.tasks[ti];
-  const int j = blockIdx.x;
-  if (j >= (int)L.K) return;
+  const u32 s = blockIdx.x;
+  if (s >= L.nstripes) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u64 bo = L.bucket_off;
-  const u64 E0 = A.E[bo + j], E1 = A.E[bo + j + 1];
-  if (E1 == E0) return;
-  const u64 d0 = (E0 + B - 1) / B * B;
-  const u64 W = (A.wr[(bo + j) * WR_STRIDE] >> 32) * (u64)B;
-  const u64 hd = d0 < E1 ? d0 : E1;     // head hole [E0, hd)
-  const u64 tl = W > hd ? W : hd;       // tail hole [tl, E1) if tl < E1
-  const u64 nhead = hd - E0;
-  const u64 ntail = tl < E1 ? E1 - tl : 0;
-  const u64 nholes = nhead + ntail;
-  const u64 o0 = E1 > d0 ? E1 : d0;
-  const u64 o = W > o0 ? W - o0 : 0;    // saved overlap elements
-  const u32 nst = L.nstripes;
-  u32 carry = 0;
-  for (u32 base = 0; base < nst; base += FILL_THREADS) {
-    u32 idx = base + threadIdx.x;
-    u32 v = idx < nst ? A.pfill[L.sbk_off + (u64)idx * L.kidx + j] : 0;
-    u32 tot;
-    u32 p = block_exclusive_scan<FILL_THREADS>(v, ws, &tot);
-    if (idx < nst) s_cum[idx] = carry + p;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) {
-    s_cum[nst] = carry;
-    // invariant of the cleanup: #holes = overlap + partial buffers (+ overflow,
-    // already moved in phase a); a violation is reported, never silent
-    if (nholes != o + carry) atomicAdd(&A.counters[4], 1u);
-  }
-  __syncthreads();
-  if (nholes == 0) return;
   char *gtask = A.base + L.t.begin * (u64)D;
-  const char *ovl = A.overlap + (bo + j) * (u64)B * D;
-  for (u64 h = threadIdx.x; h < nholes; h += FILL_THREADS) {
-    const u64 pos = h < nhead ? E0 + h : tl + (h - nhead);
-    const char *src;
-    if (h < o) {
-      src = ovl + h * D;
-    } else {
-      const u32 g = (u32)(h - o);
-      int lo = 0, hi = (int)nst;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (s_cum[mid] <= g) lo = mid + 1;
-        else hi = mid;
+  for (int j = wid; j < (int)L.K; j += NW) {
+    const u64 slot = L.sbk_off + (u64)s * L.kidx + j;
+    const u32 f = A.pfill[slot];
+    const u64 E0 = A.E[bo + j], E1 = A.E[bo + j + 1];
+    const u64 d0 = (E0 + B - 1) / B * B;
+    const u64 W = (A.wr[(bo + j) * WR_STRIDE] >> 32) * (u64)B;
+    const u64 hd = d0 < E1 ? d0 : E1;  // head hole [E0, hd)
+    const u64 tl = W > hd ? W : hd;    // tail hole [tl, E1)
+    const u64 nhead = hd - E0;
+    const u64 o0 = E1 > d0 ? E1 : d0;
+    const u64 o = W > o0 ? W - o0 : 0;  // saved overlap elements
+    auto hole = [&](u64 h) -> u64 { return h < nhead ? E0 + h : tl + (h - nhead); };
+    if (s == 0 && o) {
+      const Unit *src = reinterpret_cast<const Unit *>(A.overlap + (bo + j) * (u64)B * D);
+      for (u64 u = lane; u < o * UPE; u += 32) {
+        const u64 e = u / UPE, w = u % UPE;
+        reinterpret_cast<Unit *>(gtask + hole(e) * D)[w] = src[u];
       }
-      const int s = lo - 1;
-      src = A.partials + ((L.sbk_off + (u64)s * L.kidx + j) * B + (g - s_cum[s])) * D;
     }
-    const Unit *su = reinterpret_cast<const Unit *>(src);
-    Unit *du = reinterpret_cast<Unit *>(gtask + pos * D);
-#pragma unroll
-    for (int w = 0; w < UPE; ++w) du[w] = su[w];
+    if (f == 0) continue;
+    const u64 h0 = o + A.pcum[slot];
+    const Unit *src = reinterpret_cast<const Unit *>(A.partials + slot * (u64)B * D);
+    for (u32 u = lane; u < f * UPE; u += 32) {
+      const u32 e = u / UPE, w = u % UPE;
+      reinterpret_cast<Unit *>(gtask + hole(h0 + e) * D)[w] = src[u];
+    }
   }
 }
 

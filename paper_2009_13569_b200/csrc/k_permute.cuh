@@ -34,9 +34,35 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
     if (idx < L.nstripes) A.fcum[L.stripe_first + idx] = carry + p;
     carry += tot;
   }
+  // per bucket: total count over the stripes and the exclusive
+  // prefix over the stripes of the partial-buffer fills (cleanup, K5b)
   u32 c = 0;
   if (j < K) {
-    for (u32 s = 0; s < L.nstripes; ++s) c += A.counts[L.sbk_off + (u64)s * L.kidx + j];
+    u32 pc = 0;
+    const u32 ns = L.nstripes;
+    u32 s = 0;
+    for (; s + 8 <= ns; s += 8) {
+      u32 cv[8], pv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const u64 slot = L.sbk_off + (u64)(s + q) * L.kidx + j;
+        cv[q] = A.counts[slot];
+        pv[q] = A.pfill[slot];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        c += cv[q];
+        A.pcum[L.sbk_off + (u64)(s + q) * L.kidx + j] = pc;
+        pc += pv[q];
+      }
+    }
+    for (; s < ns; ++s) {
+      const u64 slot = L.sbk_off + (u64)s * L.kidx + j;
+      c += A.counts[slot];
+      A.pcum[slot] = pc;
+      pc += A.pfill[slot];
+    }
+    A.ptot[L.bucket_off + j] = pc;
   }
   u32 total;
   u32 pre = block_exclusive_scan<BND_THREADS>(c, ws, &total);
@@ -167,6 +193,7 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
 // byte with acquire loads.  Same guarantee, no shared counters, no fences
 // (DESIGN "Permutation on the GPU").
 constexpr int PERM_WARPS = 8;
+constexpr u32 PERM_HOP_WINDOW = 64;  // tasks an idle agent may look ahead
 #ifndef IPS4O_PERM_DIGIT_PACE_NS
 #define IPS4O_PERM_DIGIT_PACE_NS 100
 #endif
@@ -272,12 +299,15 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
   for (u32 hop = 0; hop < A.ntasks; ++hop) {
     if (hop > 0) {
       if (A.dbg_one_agent) break;
-      // next unfinished task after ti (32 done flags per probe)
+      // next unfinished task among the following PERM_HOP_WINDOW tasks (32
+      // done flags per probe; a bounded window keeps levels with thousands of
+      // small tasks from scanning all of them)
       u32 nxt = ~0u;
-      for (u32 base = 1; base < A.ntasks && nxt == ~0u; base += 32) {
+      const u32 lim = A.ntasks < PERM_HOP_WINDOW + 1 ? A.ntasks : PERM_HOP_WINDOW + 1;
+      for (u32 base = 1; base < lim && nxt == ~0u; base += 32) {
         u32 q = ti + base + lane;
         q = q >= A.ntasks ? q - A.ntasks : q;
-        const bool open = base + lane < A.ntasks && ld_relaxed_u32(&A.task_done[q]) == 0;
+        const bool open = base + lane < lim && ld_relaxed_u32(&A.task_done[q]) == 0;
         const unsigned m = __ballot_sync(0xffffffffu, open);
         if (m) nxt = __shfl_sync(0xffffffffu, q, __ffs(m) - 1);
       }

@@ -139,13 +139,21 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   const int m = (int)L.m;
   const int P = next_pow2_i(m) > SORT_THREADS ? next_pow2_i(m) : SORT_THREADS;
   // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9)
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    Key v = key_max<Key>();
-    if (i < m) {
-      u64 idx = sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i);
-      v = Tr::key(A.base + idx * Tr::D);
+  {
+    // all of a thread's sample loads are issued before any is used
+    constexpr int MAXE = sample_max<DT>() / SAMPLE_THREADS;
+    Key v[MAXE];
+#pragma unroll
+    for (int q = 0; q < MAXE; ++q) {
+      const int i = threadIdx.x + q * SAMPLE_THREADS;
+      v[q] = key_max<Key>();
+      if (i < m) v[q] = Tr::key(A.base + sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i) * Tr::D);
     }
-    s_keys[i] = v;
+#pragma unroll
+    for (int q = 0; q < MAXE; ++q) {
+      const int i = threadIdx.x + q * SAMPLE_THREADS;
+      if (i < P) s_keys[i] = v[q];
+    }
   }
   __syncthreads();
   switch (P / SORT_THREADS) {

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--base-cap", type=int, default=0)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--max-levels", type=int, default=0)
+    ap.add_argument("--alpha-min", type=int, default=0)
     ap.add_argument("--nexact", type=int, default=0, help="element count (overrides --n)")
     a = ap.parse_args()
     import numpy as np
@@ -33,7 +34,7 @@ def main():
     algo = ips.DIGIT if a.algo == "digit" else ips.TREE
     for r in range(a.reps):
         work.copy_(src)
-        st = ips.sort_ex(work, dt, algo=algo, base_cap=a.base_cap, timing=True, max_levels=a.max_levels)
+        st = ips.sort_ex(work, dt, algo=algo, base_cap=a.base_cap, timing=True, max_levels=a.max_levels, alpha_min=a.alpha_min)
         torch.cuda.synchronize()
         print(r, {k: round(v, 3) for k, v in st["kernel_ms"].items() if v}, st["levels"], st["tasks_per_level"])
     if a.check and dt == 0:
