@@ -215,7 +215,7 @@ template <int DT, int ALGO> static int set_attrs() {
   CK(cudaFuncSetAttribute(basecase_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)BaseSmem<DT>::bytes));
   CK(cudaFuncSetAttribute(sample_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)(sample_max<DT>() * sizeof(typename Traits<DT>::Key))));
+                          (int)sample_smem<DT>()));
   CK(cudaFuncSetAttribute(stripe_fix_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   done = true;
   return 0;
@@ -368,8 +368,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
 
   // K1 sampling + tree (or digit setup)
   {
-    int pw = (int)next_pow2_u64(std::max<u32>(P.max_m, SORT_THREADS));
-    size_t sm = ALGO == ALGO_TREE ? (size_t)pw * sizeof(Key) : 0;
+    size_t sm = ALGO == ALGO_TREE ? sample_smem<DT>() : 0;
     sample_kernel<DT, ALGO><<<(unsigned)T, SAMPLE_THREADS, sm, c.st>>>(A);
     CKLAUNCH();
     if ((rc = mark(c, KF_SAMPLE))) return rc;

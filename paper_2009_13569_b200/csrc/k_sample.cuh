@@ -9,6 +9,10 @@ namespace ips4o {
 constexpr int SAMPLE_THREADS = 1024;  // = SORT_THREADS
 // at most 16 keys per thread of the register sort (4 for 16-byte keys)
 template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 16384; }
+// dynamic shared memory of sample_kernel: the samples + 16-bit digit counters
+template <int DT> __host__ __device__ constexpr size_t sample_smem() {
+  return (size_t)sample_max<DT>() * sizeof(typename Traits<DT>::Key) + (sizeof(typename Traits<DT>::Key) == 8 ? 16384 : 4096) * 2;
+}
 
 __host__ __device__ __forceinline__ int next_pow2_i(int x) {
   int p = 1;
@@ -131,64 +135,181 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   }
   extern __shared__ __align__(16) char smem_raw[];
   Key *s_keys = reinterpret_cast<Key *>(smem_raw);
-  __shared__ Key s_cand[256];
-  __shared__ int s_u, s_leaves;
+  u32 *s_hist = reinterpret_cast<u32 *>(smem_raw + (size_t)sample_max<DT>() * sizeof(Key));
+  const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);
+  __shared__ Key s_cand[256], s_pick[256], s_red[2][32];
+  __shared__ u32 s_ws[SAMPLE_THREADS / 32 + 1];
+  __shared__ int s_u, s_leaves, s_k, s_slow;
   Key *tree = reinterpret_cast<Key *>(A.trees) + (size_t)ti * 2 * Tr::KIDX;
   Key *spl = tree + Tr::KIDX;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NT = SAMPLE_THREADS;
+  constexpr int MAXE = sample_max<DT>() / NT;
+  constexpr int DB = sizeof(Key) == 8 ? 14 : 12;  // digit bits: 2^DB >= sample_max
+  static_assert((1 << DB) >= sample_max<DT>(), "one digit per sample");
+  constexpr int RUNMAX = 32;                       // longer runs: full sort instead
 
   const int m = (int)L.m;
   const int P = next_pow2_i(m) > SORT_THREADS ? next_pow2_i(m) : SORT_THREADS;
-  // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9)
-  {
-    // all of a thread's sample loads are issued before any is used
-    constexpr int MAXE = sample_max<DT>() / SAMPLE_THREADS;
-    Key v[MAXE];
+  // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9);
+  // all of a thread's sample loads are issued before any is used
+  Key v[MAXE];
+  Key kmin = key_max<Key>(), kmax = (Key)0;
 #pragma unroll
-    for (int q = 0; q < MAXE; ++q) {
-      const int i = threadIdx.x + q * SAMPLE_THREADS;
-      v[q] = key_max<Key>();
-      if (i < m) v[q] = Tr::key(A.base + sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i) * Tr::D);
+  for (int q = 0; q < MAXE; ++q) {
+    const int i = tid + q * NT;
+    v[q] = key_max<Key>();
+    if (i < m) {
+      v[q] = Tr::key(A.base + sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i) * Tr::D);
+      kmin = v[q] < kmin ? v[q] : kmin;
+      kmax = v[q] > kmax ? v[q] : kmax;
     }
+  }
+  // The picks only need the sample's order statistics at k'-1 ranks: a
+  // counting sort by a digit scaled to the sample's range (~1 sample per
+  // digit, the same digit as the base case) puts every sample into its run,
+  // and each pick ranks the few samples of its run.  Exact: the same
+  // elements a full sort would put at those ranks.
 #pragma unroll
-    for (int q = 0; q < MAXE; ++q) {
-      const int i = threadIdx.x + q * SAMPLE_THREADS;
-      if (i < P) s_keys[i] = v[q];
+  for (int o = 16; o > 0; o >>= 1) {
+    const Key a = shfl_xor_k<Key>(kmin, o), b = shfl_xor_k<Key>(kmax, o);
+    kmin = a < kmin ? a : kmin;
+    kmax = b > kmax ? b : kmax;
+  }
+  if (lane == 0) {
+    s_red[0][wid] = kmin;
+    s_red[1][wid] = kmax;
+  }
+  for (int w = tid; w < (1 << DB) / 2; w += NT) s_hist[w] = 0;
+  if (tid == 0) s_slow = 0;
+  __syncthreads();
+  kmin = s_red[0][0];
+  kmax = s_red[1][0];
+  for (int w = 1; w < NT / 32; ++w) {
+    kmin = s_red[0][w] < kmin ? s_red[0][w] : kmin;
+    kmax = s_red[1][w] > kmax ? s_red[1][w] : kmax;
+  }
+  int lg = 1;
+  while ((1 << lg) < m && lg < DB) ++lg;
+  const Key range = kmax - kmin;
+  const int bits = bitlen(range);
+  const int ds = bits > 32 ? bits - 32 : 0;
+  const u32 r32 = (u32)(range >> ds);
+  const bool direct = r32 < (1u << lg);
+  const u32 dmul = direct ? 1u : (u32)((1ull << (32 + lg)) / ((u64)r32 + 1));
+  const int nd = direct ? (int)r32 + 1 : (1 << lg);
+  auto digit = [&](const Key &x) -> u32 {
+    const u32 w = (u32)((x - kmin) >> ds);
+    return direct ? w : __umulhi(w, dmul);
+  };
+#pragma unroll
+  for (int q = 0; q < MAXE; ++q)
+    if (tid + q * NT < m) {
+      const u32 d = digit(v[q]);
+      atomicAdd(&s_hist[d >> 1], 1u << ((d & 1) << 4));
+    }
+  __syncthreads();
+  {
+    constexpr int WPT = ((1 << DB) / 2 + NT - 1) / NT;
+    u32 h[WPT], tot = 0;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      h[q] = s_hist[tid * WPT + q];
+      tot += (h[q] & 0xFFFFu) + (h[q] >> 16);
+    }
+    u32 all;
+    u32 st = block_exclusive_scan<NT>(tot, s_ws, &all);
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const u32 c0 = h[q] & 0xFFFFu, c1 = h[q] >> 16;
+      s_hist[tid * WPT + q] = st | ((st + c0) << 16);
+      st += c0 + c1;
     }
   }
   __syncthreads();
-  switch (P / SORT_THREADS) {
-    case 1: bitonic_sort_reg<Key, 1>(s_keys); break;
-    case 2: bitonic_sort_reg<Key, 2>(s_keys); break;
-    case 4: bitonic_sort_reg<Key, 4>(s_keys); break;
-    default:
-      if constexpr (sizeof(Key) == 8) {
-        if (P == 8 * SORT_THREADS) bitonic_sort_reg<Key, 8>(s_keys);
-        else bitonic_sort_reg<Key, 16>(s_keys);
+#pragma unroll
+  for (int q = 0; q < MAXE; ++q)
+    if (tid + q * NT < m) {
+      const u32 d = digit(v[q]);
+      const int sh = (d & 1) << 4;
+      const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
+      s_keys[(old >> sh) & 0xFFFFu] = v[q];
+    }
+  __syncthreads();  // s_end[d] = end of run d
+  // element of rank p among the samples; flags the slow path for long runs
+  auto pick = [&](int p) -> Key {
+    int lo = 0, hi = nd - 1;  // smallest d with end(d) > p
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int)s_end[mid] > p) hi = mid;
+      else lo = mid + 1;
+    }
+    const int a = lo ? (int)s_end[lo - 1] : 0, b = (int)s_end[lo];
+    if (b - a > RUNMAX) {
+      s_slow = 1;
+      return (Key)0;
+    }
+    for (int i = a; i < b; ++i) {
+      const Key x = s_keys[i];
+      int r = 0;
+      for (int j = a; j < b; ++j) {
+        const Key y = s_keys[j];
+        r += (y < x || (y == x && j < i)) ? 1 : 0;
       }
-      break;
-  }
+      if (r == p - a) return x;
+    }
+    return (Key)0;  // not reached
+  };
+  const bool all_equal = !(kmin < kmax);
 
-  if (threadIdx.x == 0) {
-    key_to_words<Key>(s_keys[0], L.lut_lo);
-    key_to_words<Key>(s_keys[m - 1], L.lut_hi);
-    // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
-    // duplicate was removed (R23); R10: halve k until the indices fit.
-    int k = (int)L.k_req;
-    const int kidx_budget = (int)L.kidx;
-    for (;;) {
-      int alpha = m / k;
+  if (tid == 0) {
+    key_to_words<Key>(kmin, L.lut_lo);
+    key_to_words<Key>(kmax, L.lut_hi);
+    s_k = (int)L.k_req;
+  }
+  // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
+  // duplicate was removed (R23); R10: halve k until the indices fit.
+  bool sorted = false;
+  for (;;) {
+    __syncthreads();
+    const int k = s_k;
+    const int alpha = m / k;
+    if (tid < k - 1) {
+      const int p = (tid + 1) * alpha - 1;
+      s_pick[tid] = all_equal ? kmin : sorted ? s_keys[p] : pick(p);
+    }
+    __syncthreads();
+    if (s_slow && !sorted) {
+      // a pick fell into a long run of near-equal keys: sort all samples
+      for (int i = m + tid; i < P; i += NT) s_keys[i] = key_max<Key>();
+      __syncthreads();
+      switch (P / SORT_THREADS) {
+        case 1: bitonic_sort_reg<Key, 1>(s_keys); break;
+        case 2: bitonic_sort_reg<Key, 2>(s_keys); break;
+        case 4: bitonic_sort_reg<Key, 4>(s_keys); break;
+        default:
+          if constexpr (sizeof(Key) == 8) {
+            if (P == 8 * SORT_THREADS) bitonic_sort_reg<Key, 8>(s_keys);
+            else bitonic_sort_reg<Key, 16>(s_keys);
+          }
+          break;
+      }
+      sorted = true;
+      continue;  // redo the picks from the sorted samples
+    }
+    if (tid == 0) {
       int u = 0, dup = 0;
       for (int j = 0; j < k - 1; ++j) {
-        Key c = s_keys[(j + 1) * alpha - 1];
+        const Key c = s_pick[j];
         if (u > 0 && s_cand[u - 1] == c) {
           dup = 1;
           continue;
         }
         s_cand[u++] = c;
       }
-      int leaves = next_pow2_i(u + 1);
-      int need = dup ? 2 * leaves : leaves;
-      if (need <= kidx_budget || k <= 2) {
+      const int leaves = next_pow2_i(u + 1);
+      const int need = dup ? 2 * leaves : leaves;
+      if (need <= (int)L.kidx || k <= 2) {
         L.K = (u32)need;
         L.l = (u32)log2_i(leaves);
         L.equality = (u32)dup;
@@ -196,10 +317,13 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
         L.shift = 0;
         s_u = u;
         s_leaves = leaves;
-        break;
+        s_k = 0;
+      } else {
+        s_k = k >> 1;
       }
-      k >>= 1;
     }
+    __syncthreads();
+    if (s_k == 0) break;
   }
   __syncthreads();
   const int u = s_u, leaves = s_leaves, s = leaves - 1;
