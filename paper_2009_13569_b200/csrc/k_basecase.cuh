@@ -17,10 +17,13 @@ namespace ips4o {
 
 template <int DT> struct BaseItem;
 
+#ifndef IPS4O_BC_THREADS
+#define IPS4O_BC_THREADS 1024
+#endif
 template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
-  static constexpr int THREADS = 1024, DBMAX = 14, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr int THREADS = IPS4O_BC_THREADS, DBMAX = 14, CAP = Traits<DT_U64>::BASE_CAP;
   static constexpr bool STAGE_RECORDS = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -184,7 +187,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     __syncthreads();
     BC_PHASE(0)
     // 1. histogram of 16-bit counters (BU independent loads in flight)
-    constexpr int BU = 8;
+#ifndef IPS4O_BC_BU
+#define IPS4O_BC_BU 4
+#endif
+    constexpr int BU = IPS4O_BC_BU;
     for (int i0 = tid; i0 < m; i0 += NT * BU) {
       Item it[BU];
 #pragma unroll
