@@ -676,10 +676,20 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     if (lhi > thi) lhi = thi;
     if (lhi < llo) lhi = llo;
   }
+  // When the sample's range covers a good part of the task's bounds, the
+  // table spans the bounds themselves: every key then maps to a slot without
+  // clamping (keys outside the sample range only in the first/last slots
+  // otherwise).
+  const bool span_task = ALGO == ALGO_TREE && (lhi - llo) >= ((thi - tlo) >> 2);
+  if (span_task) {
+    llo = tlo;
+    lhi = thi;
+  }
   int ls = bitlen((Key)(lhi - llo)) - S::LUT_BITS;
   if (ls < 0) ls = 0;
   const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
   const int nspl = (1 << l) - 1;
+  constexpr u32 FIN = 1u << 31;  // table entry holds the final bucket
   if (ALGO == ALGO_TREE) {
     __syncthreads();
     auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
@@ -699,7 +709,9 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
         // a = #{splitters < r0}; the count covers splitters in [r0, r1] (a
         // slot with none cannot hold a key equal to a splitter)
         const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
-        e = a | ((b - a) << 16);
+        // no splitter in the slot: no key in it equals one, so key < s_a,
+        // except above the last splitter (bucket 2s+1 with equality buckets)
+        e = b == a ? FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | ((b - a) << 16);
       }
       s_lut[q] = e;
     }
@@ -760,24 +772,28 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
           const Key dk = key[k] - llo;
-          u32 q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
+          u32 q;
+          if (span_task) {
+            // keys lie in [tlo, thi]; the clamp only guards the unused lanes
+            // of a partial tile
+            q = min((u32)(dk >> ls), nlut_used - 1);
+          } else {
+            q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
+          }
           ent[k] = s_lut[q];
         }
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
-          u32 a = ent[k] & 0xFFFFu;
-          const u32 c = ent[k] >> 16;
-          if (c) {  // the slot holds splitters: lower bound among them
-            u32 b = a + c;
+          if (ent[k] & FIN) {
+            bkt[k] = ent[k] & 0xFFFFu;
+          } else {  // the slot holds splitters: lower bound among them
+            u32 a = ent[k] & 0xFFFFu, b = a + (ent[k] >> 16);
             while (a < b) {
               const u32 mid = (a + b) >> 1;
               if (s_spl[mid] < key[k]) a = mid + 1;
               else b = mid;
             }
             bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
-          } else {  // no splitter in the slot: no key here equals one, so
-                    // key < s_a, except above the last splitter (bucket 2s+1)
-            bkt[k] = eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a;
           }
         }
       } else {
