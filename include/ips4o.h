@@ -35,6 +35,8 @@ extern "C" {
  *   IPS4O_REC100_KEY10  100 B record, key = bytes 0..9 compared
  *                       lexicographically as unsigned bytes (Alg. 4), payload
  *                       bytes 10..99 carried along.
+ *   IPS4O_U32           4 B, unsigned 32-bit key, ascending unsigned order
+ *                       ("32-bit unsigned integers").
  * The sort is NOT stable (the block permutation P:840-922 moves whole blocks
  * in arbitrary order; DESIGN R3): for PAIR and REC100 the order inside a run
  * of equal keys is unspecified. */
@@ -42,7 +44,8 @@ enum ips4o_dtype {
     IPS4O_U64 = 0,
     IPS4O_F64 = 1,
     IPS4O_PAIR_U64_U64 = 2,
-    IPS4O_REC100_KEY10 = 3
+    IPS4O_REC100_KEY10 = 3,
+    IPS4O_U32 = 4
 };
 
 /* Classifier of the partitioning step. */

@@ -23,6 +23,7 @@ size_t orc_elem_bytes(int dtype)
     case ORC_F64: return 8;
     case ORC_PAIR: return 16;
     case ORC_REC100: return 100;
+    case ORC_U32: return 4;
     default: return 0;
     }
 }
@@ -33,6 +34,15 @@ static int less_u64(const void *a, const void *b)
     uint64_t x, y;
     memcpy(&x, a, 8);
     memcpy(&y, b, 8);
+    return x < y;
+}
+
+/* unsigned 32-bit '<' */
+static int less_u32(const void *a, const void *b)
+{
+    uint32_t x, y;
+    memcpy(&x, a, 4);
+    memcpy(&y, b, 4);
     return x < y;
 }
 
@@ -74,6 +84,7 @@ static less_fn less_of(int dtype)
     case ORC_F64: return less_f64;
     case ORC_PAIR: return less_pair;
     case ORC_REC100: return less_rec100;
+    case ORC_U32: return less_u32;
     default: return 0;
     }
 }
@@ -224,7 +235,7 @@ int64_t orc_parity_check(const void *g, const void *o, uint64_t n, int dtype)
     size_t D = orc_elem_bytes(dtype);
     const unsigned char *G = (const unsigned char *)g;
     const unsigned char *O = (const unsigned char *)o;
-    if (dtype == ORC_U64 || dtype == ORC_F64) {
+    if (dtype == ORC_U64 || dtype == ORC_F64 || dtype == ORC_U32) {
         for (uint64_t i = 0; i < n; i++)
             if (memcmp(G + i * D, O + i * D, D) != 0) return (int64_t)i;
         return -1;
@@ -394,7 +405,13 @@ uint32_t orc_radix_digit(int dtype, const void *e, int shift, int bits)
         return d;
     }
     uint64_t key;
-    memcpy(&key, c, 8);
+    if (dtype == ORC_U32) {
+        uint32_t k32;
+        memcpy(&k32, c, 4);
+        key = k32;
+    } else {
+        memcpy(&key, c, 8);
+    }
     if (dtype == ORC_F64) {
         /* Non-negative doubles order like their magnitude bits and come after
          * all negatives: key = 2^63 + mag.  Negative doubles order by

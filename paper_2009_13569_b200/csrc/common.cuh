@@ -53,6 +53,19 @@ template <> struct Traits<DT_F64> {
   }
 };
 
+template <> struct Traits<DT_U32> {
+  static constexpr int D = 4;
+  using Key = u64;                  // zero-extended: the 64-bit key machinery applies
+  using Unit = u32;
+  static constexpr int B = 128;     // 512 B blocks
+  static constexpr int KIDX = 256;
+  static constexpr int BASE_CAP = 32768;
+  static constexpr int CLS_THREADS = 512;
+  static constexpr int CLS_TILE = 4096;
+  static constexpr int KEY_UNITS = 1;
+  __device__ __forceinline__ static Key key(const char *e) { return *reinterpret_cast<const u32 *>(e); }
+};
+
 template <> struct Traits<DT_PAIR> {
   static constexpr int D = 16;
   using Key = u64;

@@ -10,7 +10,7 @@ typedef unsigned int u32;
 typedef long long i64;
 typedef unsigned __int128 u128;
 
-enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3 };
+enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3, DT_U32 = 4 };
 enum { ALGO_TREE = 0, ALGO_DIGIT = 1 };
 
 // Flags of a task.

@@ -293,6 +293,9 @@ template <int DT> static void key_to_raw(const u64 *w, unsigned char *out) {
   } else if (DT == DT_F64) {
     u64 b = key_to_f64(w[0]);
     memcpy(out, &b, 8);
+  } else if (DT == DT_U32) {
+    u32 b = (u32)w[0];
+    memcpy(out, &b, 4);
   } else {
     memcpy(out, &w[0], 8);
   }
@@ -303,6 +306,11 @@ template <int DT> static void raw_to_key(const unsigned char *in, u64 *w) {
     for (int i = 0; i < 10; ++i) k = (k << 8) | in[i];
     w[0] = (u64)k;
     w[1] = (u64)(k >> 64);
+  } else if (DT == DT_U32) {
+    u32 b;
+    memcpy(&b, in, 4);
+    w[0] = b;
+    w[1] = 0;
   } else {
     u64 b;
     memcpy(&b, in, 8);
@@ -652,6 +660,7 @@ static int dtype_bytes(int dtype) {
     case DT_F64: return 8;
     case DT_PAIR: return 16;
     case DT_REC100: return 100;
+    case DT_U32: return 4;
     default: return 0;
   }
 }
@@ -750,6 +759,7 @@ int ips4o_sort_ex(void *ptr, uint64_t n, int dtype, void *stream, const ips4o_op
     case DT_F64: rc = sort_impl<DT_F64>(c, base, n, nullptr); break;
     case DT_PAIR: rc = sort_impl<DT_PAIR>(c, base, n, nullptr); break;
     case DT_REC100: rc = sort_impl<DT_REC100>(c, base, n, nullptr); break;
+    case DT_U32: rc = sort_impl<DT_U32>(c, base, n, nullptr); break;
   }
   finish_ctx(c, rc);
   return rc;
@@ -841,6 +851,7 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
     case DT_U64: B = Traits<DT_U64>::B; KI = Traits<DT_U64>::KIDX; M = Traits<DT_U64>::BASE_CAP; break;
     case DT_F64: B = Traits<DT_F64>::B; KI = Traits<DT_F64>::KIDX; M = Traits<DT_F64>::BASE_CAP; break;
     case DT_PAIR: B = Traits<DT_PAIR>::B; KI = Traits<DT_PAIR>::KIDX; M = Traits<DT_PAIR>::BASE_CAP; break;
+    case DT_U32: B = Traits<DT_U32>::B; KI = Traits<DT_U32>::KIDX; M = Traits<DT_U32>::BASE_CAP; break;
     default: B = Traits<DT_REC100>::B; KI = Traits<DT_REC100>::KIDX; M = Traits<DT_REC100>::BASE_CAP; keyb = 16; break;
   }
   if (opt && opt->base_cap > 0 && (u64)opt->base_cap < M) M = (u64)opt->base_cap;
@@ -899,12 +910,13 @@ int ips4o_get_dtype_info(int dtype, ips4o_dtype_info *out) {
   out->block_elems = Traits<DTc>::B;              \
   out->kidx_max = Traits<DTc>::KIDX;              \
   out->base_cap = Traits<DTc>::BASE_CAP;          \
-  out->key_bytes = DTc == DT_REC100 ? 16 : 8;     \
+  out->key_bytes = DTc == DT_REC100 ? 16 : DTc == DT_U32 ? 4 : 8; \
   return IPS4O_OK;
     case DT_U64: FILL(DT_U64)
     case DT_F64: FILL(DT_F64)
     case DT_PAIR: FILL(DT_PAIR)
     case DT_REC100: FILL(DT_REC100)
+    case DT_U32: FILL(DT_U32)
 #undef FILL
     default: return IPS4O_ERR_INVALID;
   }
@@ -918,13 +930,14 @@ int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream, const i
   Ctx c;
   int rc = init_ctx(c, stream, opt, nullptr);
   if (rc) return rc;
-  StepCapture cap{info, dtype == DT_REC100 ? 16 : 8};
+  StepCapture cap{info, dtype == DT_REC100 ? 16 : dtype == DT_U32 ? 4 : 8};
   char *base = reinterpret_cast<char *>(ptr);
   switch (dtype) {
     case DT_U64: rc = sort_impl<DT_U64>(c, base, n, &cap); break;
     case DT_F64: rc = sort_impl<DT_F64>(c, base, n, &cap); break;
     case DT_PAIR: rc = sort_impl<DT_PAIR>(c, base, n, &cap); break;
     case DT_REC100: rc = sort_impl<DT_REC100>(c, base, n, &cap); break;
+    case DT_U32: rc = sort_impl<DT_U32>(c, base, n, &cap); break;
   }
   if (rc == 0) {
     cudaError_t e = cudaStreamSynchronize(c.st);
@@ -941,7 +954,7 @@ template <int DT>
 static int classify_impl(const void *elems, u64 n, const unsigned char *raw, int u, int eq, u32 *out,
                          cudaStream_t st) {
   using Key = typename Traits<DT>::Key;
-  const int kb = DT == DT_REC100 ? 16 : 8;
+  const int kb = DT == DT_REC100 ? 16 : DT == DT_U32 ? 4 : 8;
   int leaves = 1;
   while (leaves < u + 1) leaves <<= 1;
   if (leaves > 256) return IPS4O_ERR_INVALID;
@@ -988,6 +1001,7 @@ extern "C" int ips4o_classify(const void *elems, uint64_t n, int dtype, const vo
     case DT_U64: return classify_impl<DT_U64>(elems, n, raw, u, equality, out, st);
     case DT_F64: return classify_impl<DT_F64>(elems, n, raw, u, equality, out, st);
     case DT_PAIR: return classify_impl<DT_PAIR>(elems, n, raw, u, equality, out, st);
+    case DT_U32: return classify_impl<DT_U32>(elems, n, raw, u, equality, out, st);
     default: return classify_impl<DT_REC100>(elems, n, raw, u, equality, out, st);
   }
 }

@@ -38,6 +38,15 @@ template <> struct BaseItem<DT_F64> {
   __device__ static Key key(const Item &it) { return it; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
 };
+template <> struct BaseItem<DT_U32> {
+  using Item = u32;
+  using Key = u64;
+  static constexpr int THREADS = 1024, DBMAX = 15, CAP = Traits<DT_U32>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = false;
+  __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u32 *>(e); }
+  __device__ static Key key(const Item &it) { return it; }
+  __device__ static bool less(const Item &a, const Item &b) { return a < b; }
+};
 struct alignas(16) PairItem {
   u64 key, val;
 };
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         }
       }
       const int pos = a + rank;
-      if constexpr (DT == DT_U64 || DT == DT_PAIR) {
+      if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32) {
         reinterpret_cast<Item *>(g)[pos] = it;
       } else if constexpr (DT == DT_F64) {
         reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);

@@ -290,6 +290,8 @@ template <int DT>
 __device__ __forceinline__ typename Traits<DT>::Key elem_key(const typename Traits<DT>::Unit &x) {
   if constexpr (DT == DT_PAIR) {
     return ((u64)x.y << 32) | (u64)x.x;
+  } else if constexpr (DT == DT_U32) {
+    return (u64)x;
   } else if constexpr (DT == DT_F64) {
     return f64_to_key(x);
   } else {
@@ -599,10 +601,10 @@ template <int DT> struct ClsV2 {
 #define IPS4O_CLS_NT 1024
 #endif
   static constexpr int NT = IPS4O_CLS_NT;
-  static constexpr int T = Tr::D == 8 ? 4096 : 2048;
+  static constexpr int T = Tr::D <= 8 ? 4096 : 2048;
   static constexpr int IPT = T / NT;
   static constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX;
-  static constexpr int BUFS = B + (Tr::D == 8 ? 1 : 0);  // buffer stride in elements (bank skew)
+  static constexpr int BUFS = B + (Tr::D <= 8 ? 1 : 0);  // buffer stride in elements (bank skew)
   static constexpr size_t off_buf = 0;
   static constexpr size_t off_stage = ((size_t)KI * BUFS * D + 15) / 16 * 16;
   static constexpr size_t off_tree = off_stage + (size_t)T * D;

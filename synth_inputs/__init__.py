@@ -141,6 +141,35 @@ def ones_u64(n: int, seed: int = 0) -> np.ndarray:
     return np.ones(n, dtype=np.uint64)
 
 
+def zero_u64(n: int, seed: int = 0) -> np.ndarray:
+    """Zero: just zeros."""
+    return np.zeros(n, dtype=np.uint64)
+
+
+def eightdup_u64(n: int, seed: int = 0) -> np.ndarray:
+    """EightDup: A[i] = (i^8 + n/2) mod n, i^8 mod n by repeated
+    squaring mod n (every square < 2^60 for n <= 2^30)."""
+    out = np.empty(n, dtype=np.uint64)
+    nn = np.uint64(max(n, 1))
+    half = np.uint64(n // 2)
+    for c0 in range(0, n, CHUNK):
+        c1 = min(n, c0 + CHUNK)
+        x = np.arange(c0, c1, dtype=np.uint64) % nn
+        for _ in range(3):
+            x = (x * x) % nn
+        out[c0:c1] = (x + half) % nn
+    return out
+
+
+def uniform_u32(n: int, seed: int) -> np.ndarray:
+    """32-bit unsigned keys: the high halves of the SplitMix64 stream."""
+    out = np.empty(n, dtype=np.uint32)
+    for c0 in range(0, n, CHUNK):
+        c1 = min(n, c0 + CHUNK)
+        out[c0:c1] = (splitmix(seed, c0, c1 - c0) >> np.uint64(32)).astype(np.uint32)
+    return out
+
+
 def pairs(n: int, seed: int) -> np.ndarray:
     """(n, 2) uint64: column 0 = key, column 1 = value = i."""
     out = np.empty((n, 2), dtype=np.uint64)
@@ -172,6 +201,9 @@ DISTRIBUTIONS = {
     "twodup_u64": ("u64", twodup_u64),
     "zipf_u64": ("u64", zipf_u64),
     "ones_u64": ("u64", ones_u64),
+    "zero_u64": ("u64", zero_u64),
+    "eightdup_u64": ("u64", eightdup_u64),
+    "uniform_u32": ("u32", uniform_u32),
     "pairs": ("pair", pairs),
     "records100": ("rec100", records100),
 }

@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 import synth_inputs as gen
-from gpu_util import F64, PAIR, REC100, U64
+from gpu_util import F64, PAIR, REC100, U32, U64
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -134,8 +134,10 @@ def test_c2_doubles(ips, orc, name):
         sampled(ips, a, g, lambda x: x)
 
 
-@pytest.mark.parametrize("name", ["rootdup_u64", "twodup_u64", "zipf_u64", "ones_u64"])
+@pytest.mark.parametrize("name", ["rootdup_u64", "twodup_u64", "zipf_u64", "ones_u64",
+                                  "eightdup_u64", "zero_u64"])
 def test_c3_duplicates(ips, orc, name):
+    """c3 (+ the paper's EightDup and Zero)."""
     n = 1 << 30
     a = gen.generate(name, n, 3)
     g = run(ips, a, U64)
@@ -147,6 +149,9 @@ def test_c3_duplicates(ips, orc, name):
         return
     if name == "ones_u64":
         assert np.all(g == 1)
+        return
+    if name == "zero_u64":
+        assert not g.any()
         return
     assert nondecreasing(g)
     if name == "zipf_u64":
@@ -162,6 +167,21 @@ def test_c3_duplicates(ips, orc, name):
         return
     assert mhash(g) == mhash(a)
     sampled(ips, a, g, lambda x: x)
+
+
+def test_u32_uniform_2p28(ips, orc):
+    """32-bit keys at 2^28: non-decreasing, identical
+    multiset, sampled order statistics, and the full oracle on a 2^22 prefix
+    sorted separately."""
+    n = 1 << 28
+    a = gen.uniform_u32(n, 6)
+    g = run(ips, a, U32)
+    assert nondecreasing(g)
+    assert mhash(g.astype(np.uint64)) == mhash(a.astype(np.uint64))
+    sampled(ips, a, g, lambda x: x)
+    b = a[: 1 << 22].copy()
+    gb = run(ips, b, U32)
+    assert orc.parity(gb, orc.sort(b, U32), U32) == -1
 
 
 def test_c4_pairs(ips, orc):

@@ -92,3 +92,15 @@ def test_pairs_and_records():
     w = gen.splitmix(5, 0, 13 * 50).reshape(50, 13).view(np.uint8).reshape(50, 104)[:, :100]
     assert np.array_equal(r, w)
     assert gen.records100(50, 5).tobytes() == r.tobytes()
+
+
+def test_eightdup_zero_u32():
+    """EightDup A[i] = (i^8 + n/2) mod n against exact Python
+    integers; Zero all zeros; 32-bit keys = high halves of the stream."""
+    for n in (16, 1000, 4099):
+        a = gen.eightdup_u64(n)
+        assert [int(v) for v in a[:300]] == [(i ** 8 + n // 2) % n for i in range(min(n, 300))]
+    assert not gen.zero_u64(1000).any()
+    u = gen.uniform_u32(1000, 7)
+    assert u.dtype == np.uint32
+    assert np.array_equal(u, (gen.uniform_u64(1000, 7) >> np.uint64(32)).astype(np.uint32))

@@ -18,7 +18,7 @@ import pytest
 import synth_inputs as gen
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-U64, F64, PAIR, REC100 = 0, 1, 2, 3
+U64, F64, PAIR, REC100, U32 = 0, 1, 2, 3, 4
 
 
 # ----------------------------------------------------------------- helpers
@@ -26,6 +26,8 @@ def py_key(dtype, rec: bytes):
     """Independent Python key functions (Alg. 3/4)."""
     if dtype == U64:
         return struct.unpack("<Q", rec)[0]
+    if dtype == U32:
+        return struct.unpack("<I", rec)[0]
     if dtype == F64:
         return struct.unpack("<d", rec)[0]
     if dtype == PAIR:
@@ -34,7 +36,7 @@ def py_key(dtype, rec: bytes):
 
 
 def to_records(arr, dtype):
-    D = {U64: 8, F64: 8, PAIR: 16, REC100: 100}[dtype]
+    D = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4}[dtype]
     b = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
     return [bytes(b[i * D:(i + 1) * D]) for i in range(b.size // D)]
 
@@ -58,6 +60,13 @@ def battery(dtype, rng):
             cases.append([np.uint64(n - i) for i in range(n)])
             cases.append([np.uint64(i % 5) for i in range(n)])
             cases.append([np.uint64(0 if i % 3 else 2**64 - 1) for i in range(n)])
+        elif dtype == U32:
+            cases.append([int(x) for x in rng.integers(0, 2**32, n, dtype=np.uint64)])
+            cases.append([7] * n)
+            cases.append([i % 2 for i in range(n)])
+            cases.append([i for i in range(n)])
+            cases.append([n - i for i in range(n)])
+            cases.append([0 if i % 3 else 2**32 - 1 for i in range(n)])
         elif dtype == F64:
             special = [-np.inf, np.inf, -1.7976931348623157e308, 1.7976931348623157e308,
                        5e-324, -5e-324, 2.2250738585072014e-308, 0.0, -1.0, 1.0, -0.5, 3.25]
@@ -90,6 +99,8 @@ def battery(dtype, rng):
 def case_to_array(case, dtype, rng):
     if dtype == U64:
         return np.array(case, dtype=np.uint64)
+    if dtype == U32:
+        return np.array(case, dtype=np.uint32)
     if dtype == F64:
         return np.array(case, dtype=np.float64)
     if dtype == PAIR:
@@ -102,7 +113,7 @@ def case_to_array(case, dtype, rng):
 
 
 # ----------------------------------------------------------------- mergesort vs brute force
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
 def test_mergesort_matches_brute_force_and_python_sorted(orc, dtype):
     """output = input in sorted order.  Stable mergesort, stable
     insertion sort and stable Python sorted() must agree byte for byte."""
@@ -119,16 +130,18 @@ def test_mergesort_matches_brute_force_and_python_sorted(orc, dtype):
         assert orc.multiset_hash(m, dtype) == orc.multiset_hash(a, dtype)
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
 def test_mergesort_all_sequences_over_three_values(orc, dtype):
     """every permutation of every multiset of size <= 7
     over <= 3 distinct values (= all sequences over {v0,v1,v2})."""
     vals = {U64: [0, 1, 2**63 + 5], F64: [-2.0, 0.0, 3.5], PAIR: [0, 1, 2**63 + 5],
-            REC100: [0, 1, 255]}[dtype]
+            REC100: [0, 1, 255], U32: [0, 1, 2**31 + 5]}[dtype]
     for n in range(0, 8):
         for seq in itertools.product(range(3), repeat=n):
             if dtype == U64:
                 a = np.array([vals[s] for s in seq], dtype=np.uint64)
+            elif dtype == U32:
+                a = np.array([vals[s] for s in seq], dtype=np.uint32)
             elif dtype == F64:
                 a = np.array([vals[s] for s in seq], dtype=np.float64)
             elif dtype == PAIR:
@@ -144,11 +157,11 @@ def test_mergesort_all_sequences_over_three_values(orc, dtype):
 
 
 # ----------------------------------------------------------------- invariants at size
-@pytest.mark.parametrize("dtype", [U64, F64])
+@pytest.mark.parametrize("dtype", [U64, F64, U32])
 def test_mergesort_vs_numpy_sort(orc, dtype):
     """Library cross-check: numpy's sort of the same input."""
     n = 1 << 18
-    a = gen.uniform_u64(n, 11) if dtype == U64 else gen.exponential_f64(n, 11)
+    a = {U64: gen.uniform_u64, F64: gen.exponential_f64, U32: gen.uniform_u32}[dtype](n, 11)
     m = orc.sort(a, dtype)
     assert np.array_equal(m, np.sort(a, kind="stable"))
 
@@ -200,7 +213,7 @@ def test_closed_form_sorted_reverse_ones(orc):
     assert np.array_equal(orc.sort(o, U64), o)
 
 
-@pytest.mark.parametrize("name", ["twodup_u64", "zipf_u64", "rootdup_u64"])
+@pytest.mark.parametrize("name", ["twodup_u64", "zipf_u64", "rootdup_u64", "eightdup_u64", "zero_u64"])
 def test_counting_sort_pin(orc, name):
     """Reduction to counting sort: values are small integers."""
     n = 1 << 17
@@ -365,6 +378,15 @@ def test_select_splitters_equality_budget(orc):
     assert 2 * leaves <= 256
     sp2, eq2, kf2 = orc.select_splitters(np.arange(m, dtype=np.uint64), 256, 256, U64)
     assert kf2 == 256 and not eq2 and sp2.size // 8 == 255
+
+
+def test_radix_digit_u32(orc):
+    """IPS2Ra digit of 32-bit keys: bits [shift, shift+bits)."""
+    rng = np.random.default_rng(5)
+    for x in rng.integers(0, 2**32, 200, dtype=np.uint64):
+        a = np.array([x], dtype=np.uint32)
+        for sh, bits in [(0, 8), (24, 8), (13, 7), (31, 1)]:
+            assert orc.radix_digit(U32, a, sh, bits) == (int(x) >> sh) & ((1 << bits) - 1)
 
 
 def test_radix_digit_orders(orc):
