@@ -761,11 +761,19 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
 #pragma unroll
       for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
       if (want_minmax) {
+        if (cnt == T) {
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          if (tid + k * NT < cnt) {
+          for (int k = 0; k < IPT; ++k) {
             kmin = key[k] < kmin ? key[k] : kmin;
             kmax = key[k] > kmax ? key[k] : kmax;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) {
+            if (tid + k * NT < cnt) {
+              kmin = key[k] < kmin ? key[k] : kmin;
+              kmax = key[k] > kmax ? key[k] : kmax;
+            }
           }
         }
       }
