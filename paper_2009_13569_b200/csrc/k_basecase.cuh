@@ -24,7 +24,7 @@ template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
   static constexpr int THREADS = IPS4O_BC_THREADS, DBMAX = 14, CAP = Traits<DT_U64>::BASE_CAP;
-  static constexpr bool STAGE_RECORDS = false;
+  static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
@@ -33,7 +33,7 @@ template <> struct BaseItem<DT_F64> {
   using Item = u64;  // order-preserving key
   using Key = u64;
   static constexpr int THREADS = 1024, DBMAX = 14, CAP = Traits<DT_F64>::BASE_CAP;
-  static constexpr bool STAGE_RECORDS = false;
+  static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
   __device__ static Key key(const Item &it) { return it; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
@@ -42,7 +42,7 @@ template <> struct BaseItem<DT_U32> {
   using Item = u32;
   using Key = u64;
   static constexpr int THREADS = 1024, DBMAX = 15, CAP = Traits<DT_U32>::BASE_CAP;
-  static constexpr bool STAGE_RECORDS = false;
+  static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u32 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
@@ -54,7 +54,7 @@ template <> struct BaseItem<DT_PAIR> {
   using Item = PairItem;
   using Key = u64;
   static constexpr int THREADS = 512, DBMAX = 14, CAP = Traits<DT_PAIR>::BASE_CAP;
-  static constexpr bool STAGE_RECORDS = false;
+  static constexpr bool STAGE_RECORDS = false, KEY_ONLY = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const PairItem *>(e); }
   __device__ static Key key(const Item &it) { return it.key; }
   __device__ static bool less(const Item &a, const Item &b) { return a.key < b.key; }
@@ -63,7 +63,7 @@ template <> struct BaseItem<DT_REC100> {
   using Item = u128;  // key80 << 16 | index of the record in the staging area
   using Key = u128;
   static constexpr int THREADS = 512, DBMAX = 11, CAP = Traits<DT_REC100>::BASE_CAP;
-  static constexpr bool STAGE_RECORDS = true;
+  static constexpr bool STAGE_RECORDS = true, KEY_ONLY = false;
   __device__ static Item load(const char *e, u32 idx) { return (Traits<DT_REC100>::key(e) << 16) | (u128)idx; }
   __device__ static Key key(const Item &it) { return it >> 16; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
@@ -113,6 +113,69 @@ __device__ void warp_bitonic_run(typename BI::Item *a, int n, int lane) {
       __syncwarp();
     }
   }
+}
+
+// A run longer than RANKMAX (SIMD warp per run): nothing to do if all its
+// keys are equal (any order of equal keys is a sorted result); for key-only
+// items a run of at most 8 distinct keys is rewritten by counting them
+// (duplicate-heavy inputs: TwoDup, EightDup); otherwise a bitonic sort.
+template <class BI>
+__device__ void warp_sort_run(typename BI::Item *a, int n, int lane) {
+  using Item = typename BI::Item;
+  using Key = typename BI::Key;
+  const Key k0 = BI::key(a[0]);
+  bool diff = false;
+  for (int i = lane; i < n; i += 32) diff |= BI::key(a[i]) != k0;
+  if (!__any_sync(0xffffffffu, diff)) return;
+  if constexpr (BI::KEY_ONLY) {
+    constexpr int MAXV = 8;
+    Key val = 0;  // lane r < MAXV holds distinct key r and its count
+    int cnt = 0, nv = 0;
+    Key prev = 0;
+    bool done = false;
+    for (int r = 0; r <= MAXV && !done; ++r) {
+      Key mn = key_max<Key>();
+      bool any = false;
+      for (int i = lane; i < n; i += 32) {
+        const Key k = BI::key(a[i]);
+        if ((r == 0 || k > prev) && k <= mn) {
+          mn = k;
+          any = true;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const Key y = __shfl_xor_sync(0xffffffffu, mn, o);
+        mn = y < mn ? y : mn;
+      }
+      if (!__any_sync(0xffffffffu, any)) {
+        done = true;
+        break;
+      }
+      if (r == MAXV) break;  // more than MAXV distinct keys
+      int c = 0;
+      for (int i = lane; i < n; i += 32) c += BI::key(a[i]) == mn ? 1 : 0;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == r) {
+        val = mn;
+        cnt = c;
+      }
+      prev = mn;
+      nv = r + 1;
+    }
+    if (done) {
+      int off = 0;
+      for (int r = 0; r < nv; ++r) {
+        const Key v = __shfl_sync(0xffffffffu, val, r);
+        const int c = __shfl_sync(0xffffffffu, cnt, r);
+        for (int i = lane; i < c; i += 32) a[off + i] = (Item)v;
+        off += c;
+      }
+      __syncwarp();
+      return;
+    }
+  }
+  warp_bitonic_run<BI>(a, n, lane);
 }
 
 #ifdef IPS4O_PHASE_TIMING
@@ -301,13 +364,13 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         for (int q = wid; q < nbig; q += NT / 32) {
           int d = (int)s_big[q];
           int a = d ? (int)s_end[d - 1] : 0;
-          warp_bitonic_run<BI>(s_items + a, (int)s_end[d] - a, lane);
+          warp_sort_run<BI>(s_items + a, (int)s_end[d] - a, lane);
         }
       } else {
         for (int d = wid; d < nd; d += NT / 32) {
           int a = d ? (int)s_end[d - 1] : 0;
           int n = (int)s_end[d] - a;
-          if (n > RANKMAX) warp_bitonic_run<BI>(s_items + a, n, lane);
+          if (n > RANKMAX) warp_sort_run<BI>(s_items + a, n, lane);
         }
       }
       if (nbig) __syncthreads();
