@@ -97,7 +97,7 @@ struct LevelArgs {
   u64 base_cap_elems;         // base-case capacity M (elements)
   u64 seed;
   u32 dbg_one_agent;          // debug: a single permutation agent per task
-  u32 pad;
+  u32 sample_p;               // K1 shared layout: sample slots (pow2 >= every task's m)
   u64 *minmax;                // [0] = min key, [1] = max key of TF_MINMAX tasks (u64 keys)
 };
 

@@ -376,7 +376,12 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
 
   // K1 sampling + tree (or digit setup)
   {
-    size_t sm = ALGO == ALGO_TREE ? sample_smem<DT>() : 0;
+    const u64 sp = next_pow2_u64(std::max<u64>(P.max_m, SORT_THREADS));
+    size_t sm = ALGO == ALGO_TREE ? sample_smem<DT>((size_t)sp) : 0;
+    if (ALGO == ALGO_TREE) {
+      // the per-level layout lives in the kernel argument (A is passed by value)
+      A.sample_p = (u32)sp;
+    }
     sample_kernel<DT, ALGO><<<(unsigned)T, SAMPLE_THREADS, sm, c.st>>>(A);
     CKLAUNCH();
     if ((rc = mark(c, KF_SAMPLE))) return rc;

@@ -9,9 +9,10 @@ namespace ips4o {
 constexpr int SAMPLE_THREADS = 1024;  // = SORT_THREADS
 // at most 16 keys per thread of the register sort (4 for 16-byte keys)
 template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 16384; }
-// dynamic shared memory of sample_kernel: the samples + 16-bit digit counters
-template <int DT> __host__ __device__ constexpr size_t sample_smem() {
-  return (size_t)sample_max<DT>() * sizeof(typename Traits<DT>::Key) + (sizeof(typename Traits<DT>::Key) == 8 ? 16384 : 4096) * 2;
+// dynamic shared memory of sample_kernel: p sample slots + 16-bit digit
+// counters (sized per launch, so levels of small tasks run 2 CTAs per SM)
+template <int DT> __host__ __device__ constexpr size_t sample_smem(size_t p = (size_t)sample_max<DT>()) {
+  return p * sizeof(typename Traits<DT>::Key) + (sizeof(typename Traits<DT>::Key) == 8 ? 16384 : 4096) * 2;
 }
 
 __host__ __device__ __forceinline__ int next_pow2_i(int x) {
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   }
   extern __shared__ __align__(16) char smem_raw[];
   Key *s_keys = reinterpret_cast<Key *>(smem_raw);
-  u32 *s_hist = reinterpret_cast<u32 *>(smem_raw + (size_t)sample_max<DT>() * sizeof(Key));
+  u32 *s_hist = reinterpret_cast<u32 *>(smem_raw + (size_t)A.sample_p * sizeof(Key));
   const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);
   __shared__ Key s_cand[256], s_pick[256], s_red[2][32];
   __shared__ u32 s_ws[SAMPLE_THREADS / 32 + 1];
