@@ -37,6 +37,9 @@ extern "C" {
  *                       bytes 10..99 carried along.
  *   IPS4O_U32           4 B, unsigned 32-bit key, ascending unsigned order
  *                       ("32-bit unsigned integers").
+ *   IPS4O_QUARTET       32 B {uint64 a, b, c; uint64 value}, key (a, b, c)
+ *                       compared lexicographically (Alg. 3, P:1824-1836;
+ *                       P:1878).
  * The sort is NOT stable (the block permutation P:840-922 moves whole blocks
  * in arbitrary order; DESIGN R3): for PAIR and REC100 the order inside a run
  * of equal keys is unspecified. */
@@ -45,7 +48,8 @@ enum ips4o_dtype {
     IPS4O_F64 = 1,
     IPS4O_PAIR_U64_U64 = 2,
     IPS4O_REC100_KEY10 = 3,
-    IPS4O_U32 = 4
+    IPS4O_U32 = 4,
+    IPS4O_QUARTET = 5
 };
 
 /* Classifier of the partitioning step. */

@@ -17,9 +17,9 @@ import subprocess
 
 import numpy as np
 
-U64, F64, PAIR, REC100, U32 = 0, 1, 2, 3, 4
-ELEM_BYTES = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4}
-DTYPE_NAMES = {"u64": U64, "f64": F64, "pair": PAIR, "rec100": REC100, "u32": U32}
+U64, F64, PAIR, REC100, U32, QUARTET = 0, 1, 2, 3, 4, 5
+ELEM_BYTES = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}
+DTYPE_NAMES = {"u64": U64, "f64": F64, "pair": PAIR, "rec100": REC100, "u32": U32, "quartet": QUARTET}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")

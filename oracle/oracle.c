@@ -24,6 +24,7 @@ size_t orc_elem_bytes(int dtype)
     case ORC_PAIR: return 16;
     case ORC_REC100: return 100;
     case ORC_U32: return 4;
+    case ORC_QUARTET: return 32;
     default: return 0;
     }
 }
@@ -64,6 +65,17 @@ static int less_pair(const void *a, const void *b)
     return x < y;
 }
 
+/* Quartet: Alg. 3 -- a, then b, then c */
+static int less_quartet(const void *l, const void *r)
+{
+    uint64_t x[3], y[3];
+    memcpy(x, l, 24);
+    memcpy(y, r, 24);
+    if (x[0] != y[0]) return x[0] < y[0];
+    if (x[1] != y[1]) return x[1] < y[1];
+    return x[2] < y[2];
+}
+
 /* 100B: Alg. 4, key bytes k[0..9] compared as unsigned bytes */
 static int less_rec100(const void *a, const void *b)
 {
@@ -85,6 +97,7 @@ static less_fn less_of(int dtype)
     case ORC_PAIR: return less_pair;
     case ORC_REC100: return less_rec100;
     case ORC_U32: return less_u32;
+    case ORC_QUARTET: return less_quartet;
     default: return 0;
     }
 }
@@ -394,6 +407,18 @@ int orc_classify_tree(const void *tree, const void *splitter, int l, int equalit
 uint32_t orc_radix_digit(int dtype, const void *e, int shift, int bits)
 {
     const unsigned char *c = (const unsigned char *)e;
+    if (dtype == ORC_QUARTET) {
+        /* key = a*2^128 + b*2^64 + c (Alg. 3 order); bit q of it */
+        uint64_t w[3];
+        memcpy(w, c, 24); /* w[0] = a (most significant), w[2] = c */
+        uint32_t d = 0;
+        for (int t = bits - 1; t >= 0; t--) {
+            int q = shift + t;
+            int bit = (int)((w[2 - q / 64] >> (q % 64)) & 1);
+            d = 2 * d + (uint32_t)bit;
+        }
+        return d;
+    }
     if (dtype == ORC_REC100) {
         /* key = sum_i k[i] * 256^(9-i); bit q lives in byte 9 - q/8 */
         uint32_t d = 0;

@@ -18,6 +18,8 @@
  *   ORC_REC100 100 bytes, key = bytes 0..9 compared lexicographically as
  *              UNSIGNED bytes (Alg. 4; DESIGN reading R1)
  *   ORC_U32    4-byte unsigned integer, compared with unsigned '<'
+ *   ORC_QUARTET 32 bytes {uint64 a, b, c; uint64 value}, key (a, b, c) compared
+ *              lexicographically (Alg. 3)
  *
  * Pinning status: every function below is pinned by
  * a -m "not gpu" test against something other than itself (brute force,
@@ -32,7 +34,7 @@
 extern "C" {
 #endif
 
-enum { ORC_U64 = 0, ORC_F64 = 1, ORC_PAIR = 2, ORC_REC100 = 3, ORC_U32 = 4 };
+enum { ORC_U64 = 0, ORC_F64 = 1, ORC_PAIR = 2, ORC_REC100 = 3, ORC_U32 = 4, ORC_QUARTET = 5 };
 
 /* Element size in bytes, 0 for an unknown dtype. */
 size_t orc_elem_bytes(int dtype);

@@ -12,14 +12,14 @@ import ctypes
 import os
 
 __all__ = [
-    "U64", "F64", "PAIR", "REC100", "U32", "TREE", "DIGIT",
+    "U64", "F64", "PAIR", "REC100", "U32", "QUARTET", "TREE", "DIGIT",
     "load", "sort", "sort_ex", "sort_host", "partition_step", "classify",
     "scratch_bytes", "dtype_info", "Options", "Stats", "IPS4OError",
 ]
 
-U64, F64, PAIR, REC100, U32 = 0, 1, 2, 3, 4
+U64, F64, PAIR, REC100, U32, QUARTET = 0, 1, 2, 3, 4, 5
 TREE, DIGIT = 0, 1
-ELEM_BYTES = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4}
+ELEM_BYTES = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}
 KERNEL_NAMES = ["prepass", "sample", "classify", "boundaries", "stripe_fix", "permute",
                 "cleanup", "schedule", "basecase", "reverse", "host_plan", "total"]
 

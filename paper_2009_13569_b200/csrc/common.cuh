@@ -23,6 +23,85 @@ __host__ __device__ __forceinline__ u64 key_to_f64(u64 k) {
 
 __device__ __forceinline__ u32 bswap32(u32 x) { return __byte_perm(x, 0, 0x0123); }
 
+// ------------------------------------------------------------------ 192-bit keys
+// Quartet keys (a, b, c) compared lexicographically (Alg. 3) are
+// the 192-bit number a*2^128 + b*2^64 + c; w[0] = c is the least significant.
+struct K192 {
+  u64 w[3];
+  __host__ __device__ __forceinline__ K192() {}
+  __host__ __device__ __forceinline__ K192(u64 x) : w{x, 0, 0} {}
+  __host__ __device__ __forceinline__ K192(u64 lo, u64 mid, u64 hi) : w{lo, mid, hi} {}
+  __host__ __device__ __forceinline__ explicit operator u64() const { return w[0]; }
+  __host__ __device__ __forceinline__ explicit operator u32() const { return (u32)w[0]; }
+};
+__host__ __device__ __forceinline__ bool operator<(const K192 &x, const K192 &y) {
+  if (x.w[2] != y.w[2]) return x.w[2] < y.w[2];
+  if (x.w[1] != y.w[1]) return x.w[1] < y.w[1];
+  return x.w[0] < y.w[0];
+}
+__host__ __device__ __forceinline__ bool operator>(const K192 &x, const K192 &y) { return y < x; }
+__host__ __device__ __forceinline__ bool operator<=(const K192 &x, const K192 &y) { return !(y < x); }
+__host__ __device__ __forceinline__ bool operator>=(const K192 &x, const K192 &y) { return !(x < y); }
+__host__ __device__ __forceinline__ bool operator==(const K192 &x, const K192 &y) {
+  return x.w[0] == y.w[0] && x.w[1] == y.w[1] && x.w[2] == y.w[2];
+}
+__host__ __device__ __forceinline__ bool operator!=(const K192 &x, const K192 &y) { return !(x == y); }
+__host__ __device__ __forceinline__ K192 operator-(const K192 &x, const K192 &y) {
+  K192 r;
+  r.w[0] = x.w[0] - y.w[0];
+  const u64 b0 = x.w[0] < y.w[0];
+  const u64 t1 = x.w[1] - y.w[1];
+  const u64 b1 = (x.w[1] < y.w[1]) | (t1 < b0);
+  r.w[1] = t1 - b0;
+  r.w[2] = x.w[2] - y.w[2] - b1;
+  return r;
+}
+__host__ __device__ __forceinline__ K192 operator+(const K192 &x, const K192 &y) {
+  K192 r;
+  r.w[0] = x.w[0] + y.w[0];
+  const u64 c0 = r.w[0] < x.w[0];
+  const u64 t1 = x.w[1] + y.w[1];
+  const u64 c1 = (t1 < x.w[1]) | ((t1 + c0) < t1);
+  r.w[1] = t1 + c0;
+  r.w[2] = x.w[2] + y.w[2] + c1;
+  return r;
+}
+__host__ __device__ __forceinline__ K192 operator|(const K192 &x, const K192 &y) {
+  return K192(x.w[0] | y.w[0], x.w[1] | y.w[1], x.w[2] | y.w[2]);
+}
+__host__ __device__ __forceinline__ K192 operator^(const K192 &x, const K192 &y) {
+  return K192(x.w[0] ^ y.w[0], x.w[1] ^ y.w[1], x.w[2] ^ y.w[2]);
+}
+__host__ __device__ __forceinline__ K192 operator&(const K192 &x, const K192 &y) {
+  return K192(x.w[0] & y.w[0], x.w[1] & y.w[1], x.w[2] & y.w[2]);
+}
+__host__ __device__ __forceinline__ K192 operator>>(const K192 &x, int s) {
+  if (s <= 0) return x;
+  if (s >= 192) return K192(0);
+  const int q = s >> 6, r = s & 63;
+  u64 in[3] = {x.w[0], x.w[1], x.w[2]};
+  K192 o(0);
+  for (int i = 0; i + q < 3; ++i) {
+    const u64 lo = in[i + q];
+    const u64 hi = (i + q + 1 < 3) ? in[i + q + 1] : 0;
+    o.w[i] = r ? (lo >> r) | (hi << (64 - r)) : lo;
+  }
+  return o;
+}
+__host__ __device__ __forceinline__ K192 operator<<(const K192 &x, int s) {
+  if (s <= 0) return x;
+  if (s >= 192) return K192(0);
+  const int q = s >> 6, r = s & 63;
+  u64 in[3] = {x.w[0], x.w[1], x.w[2]};
+  K192 o(0);
+  for (int i = 2; i - q >= 0; --i) {
+    const u64 hi = in[i - q];
+    const u64 lo = (i - q - 1 >= 0) ? in[i - q - 1] : 0;
+    o.w[i] = r ? (hi << r) | (lo >> (64 - r)) : hi;
+  }
+  return o;
+}
+
 template <int DT> struct Traits;
 
 template <> struct Traits<DT_U64> {
@@ -66,6 +145,22 @@ template <> struct Traits<DT_U32> {
   __device__ __forceinline__ static Key key(const char *e) { return *reinterpret_cast<const u32 *>(e); }
 };
 
+template <> struct Traits<DT_QUARTET> {
+  static constexpr int D = 32;       // {u64 a, b, c; u64 value}, key (a, b, c)
+  using Key = K192;
+  using Unit = uint4;
+  static constexpr int B = 16;       // 512 B blocks
+  static constexpr int KIDX = 256;
+  static constexpr int BASE_CAP = 6144;
+  static constexpr int CLS_THREADS = 512;
+  static constexpr int CLS_TILE = 1024;
+  static constexpr int KEY_UNITS = 2;
+  __device__ __forceinline__ static Key key(const char *e) {
+    const u64 *q = reinterpret_cast<const u64 *>(e);
+    return K192(q[2], q[1], q[0]);
+  }
+};
+
 template <> struct Traits<DT_PAIR> {
   static constexpr int D = 16;
   using Key = u64;
@@ -103,11 +198,22 @@ template <> __host__ __device__ __forceinline__ u64 key_from_words<u64>(const u6
 template <> __host__ __device__ __forceinline__ u128 key_from_words<u128>(const u64 *w) {
   return ((u128)w[1] << 64) | (u128)w[0];
 }
+template <> __host__ __device__ __forceinline__ K192 key_from_words<K192>(const u64 *w) { return K192(w[0], w[1], w[2]); }
 template <class K> __host__ __device__ __forceinline__ void key_to_words(K k, u64 *w);
-template <> __host__ __device__ __forceinline__ void key_to_words<u64>(u64 k, u64 *w) { w[0] = k; w[1] = 0; }
+template <> __host__ __device__ __forceinline__ void key_to_words<u64>(u64 k, u64 *w) {
+  w[0] = k;
+  w[1] = 0;
+  w[2] = 0;
+}
 template <> __host__ __device__ __forceinline__ void key_to_words<u128>(u128 k, u64 *w) {
   w[0] = (u64)k;
   w[1] = (u64)(k >> 64);
+  w[2] = 0;
+}
+template <> __host__ __device__ __forceinline__ void key_to_words<K192>(K192 k, u64 *w) {
+  w[0] = k.w[0];
+  w[1] = k.w[1];
+  w[2] = k.w[2];
 }
 
 __device__ __forceinline__ int bitlen(u64 x) { return x ? 64 - __clzll((long long)x) : 0; }
@@ -117,10 +223,15 @@ __device__ __forceinline__ int bitlen(u128 x) {
 }
 __device__ __forceinline__ u32 digit_of(u64 x, int shift, u32 mask) { return (u32)(x >> shift) & mask; }
 __device__ __forceinline__ u32 digit_of(u128 x, int shift, u32 mask) { return (u32)(x >> shift) & mask; }
+__device__ __forceinline__ int bitlen(const K192 &x) {
+  return x.w[2] ? 128 + bitlen(x.w[2]) : x.w[1] ? 64 + bitlen(x.w[1]) : bitlen(x.w[0]);
+}
+__device__ __forceinline__ u32 digit_of(const K192 &x, int shift, u32 mask) { return (u32)(x >> shift) & mask; }
 
 template <class K> __host__ __device__ __forceinline__ K key_max();
 template <> __host__ __device__ __forceinline__ u64 key_max<u64>() { return ~0ull; }
 template <> __host__ __device__ __forceinline__ u128 key_max<u128>() { return (((u128)1) << 80) - 1; }
+template <> __host__ __device__ __forceinline__ K192 key_max<K192>() { return K192(~0ull, ~0ull, ~0ull); }
 
 // ------------------------------------------------------------------ RNG (DESIGN R8)
 constexpr u64 GAMMA = 0x9E3779B97F4A7C15ull;

@@ -10,7 +10,8 @@ typedef unsigned int u32;
 typedef long long i64;
 typedef unsigned __int128 u128;
 
-enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3, DT_U32 = 4 };
+enum { DT_U64 = 0, DT_F64 = 1, DT_PAIR = 2, DT_REC100 = 3, DT_U32 = 4, DT_QUARTET = 5 };
+constexpr int KEY_WORDS = 3;  // internal keys up to 192 bits (Quartet), [0] = least significant
 enum { ALGO_TREE = 0, ALGO_DIGIT = 1 };
 
 // Flags of a task.
@@ -26,8 +27,8 @@ enum : u32 {
 struct TaskDesc {
   u64 begin;
   u64 size;
-  u64 lo[2];  // [0] = low 64 bits, [1] = high bits
-  u64 hi[2];
+  u64 lo[KEY_WORDS];  // [0] = low 64 bits, [1], [2] = higher bits
+  u64 hi[KEY_WORDS];
   u32 level;
   u32 flags;
 };
@@ -57,8 +58,8 @@ struct LevelTask {
   int shift;         // digit shift (DIGIT)
   u32 k_used;        // k after the equality-budget rule (DESIGN R10)
   u32 pad1;
-  u64 lut_lo[2];     // key range of the sample (TREE): the classifier's lookup
-  u64 lut_hi[2];     // table spans [lut_lo, lut_hi] inside [t.lo, t.hi]
+  u64 lut_lo[KEY_WORDS];  // key range of the sample (TREE): the classifier's lookup
+  u64 lut_hi[KEY_WORDS];     // table spans [lut_lo, lut_hi] inside [t.lo, t.hi]
 };
 
 // Device pointers of one level's scratch arrays (all in one arena).
@@ -111,8 +112,8 @@ constexpr int WR_STRIDE = 8;      // u64 words per bucket slot (64 B): [0]=wr, [
 struct PrepassOut {
   u32 nondecreasing;  // all adjacent pairs a[i] <= a[i+1]
   u32 nonincreasing;  // all adjacent pairs a[i] >= a[i+1]
-  u64 minkey[2];
-  u64 maxkey[2];
+  u64 minkey[KEY_WORDS];
+  u64 maxkey[KEY_WORDS];
 };
 
 }  // namespace ips4o

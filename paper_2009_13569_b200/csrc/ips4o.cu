@@ -205,7 +205,7 @@ template <int DT> static int perm_occupancy() {
 template <int DT, int ALGO> static int set_attrs() {
   static bool done = false;
   if (done) return 0;
-  if constexpr (DT == DT_REC100) {
+  if constexpr (Traits<DT>::D > 16) {
     CK(cudaFuncSetAttribute(classify_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ClsSmem<DT>::bytes));
   } else {
@@ -296,6 +296,10 @@ template <int DT> static void key_to_raw(const u64 *w, unsigned char *out) {
   } else if (DT == DT_U32) {
     u32 b = (u32)w[0];
     memcpy(out, &b, 4);
+  } else if (DT == DT_QUARTET) {  // raw key = element bytes 0..23: a, b, c
+    memcpy(out, &w[2], 8);
+    memcpy(out + 8, &w[1], 8);
+    memcpy(out + 16, &w[0], 8);
   } else {
     memcpy(out, &w[0], 8);
   }
@@ -306,16 +310,23 @@ template <int DT> static void raw_to_key(const unsigned char *in, u64 *w) {
     for (int i = 0; i < 10; ++i) k = (k << 8) | in[i];
     w[0] = (u64)k;
     w[1] = (u64)(k >> 64);
+    w[2] = 0;
   } else if (DT == DT_U32) {
     u32 b;
     memcpy(&b, in, 4);
     w[0] = b;
     w[1] = 0;
+    w[2] = 0;
+  } else if (DT == DT_QUARTET) {
+    memcpy(&w[2], in, 8);
+    memcpy(&w[1], in + 8, 8);
+    memcpy(&w[0], in + 16, 8);
   } else {
     u64 b;
     memcpy(&b, in, 8);
     w[0] = DT == DT_F64 ? f64_to_key(b) : b;
     w[1] = 0;
+    w[2] = 0;
   }
 }
 
@@ -387,7 +398,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
     if ((rc = mark(c, KF_SAMPLE))) return rc;
   }
   // K2 classification + block flush
-  if constexpr (DT == DT_REC100) {
+  if constexpr (Traits<DT>::D > 16) {
     classify_kernel<DT, ALGO><<<(unsigned)S, Tr::CLS_THREADS, ClsSmem<DT>::bytes, c.st>>>(A);
   } else {
     classify_v2_kernel<DT, ALGO><<<(unsigned)S, ClsV2<DT>::NT, ClsV2<DT>::bytes, c.st>>>(A);
@@ -490,7 +501,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
       CK(cudaMemcpy(tr.data(), A.trees, 2 * KI * sizeof(Key), cudaMemcpyDeviceToHost));
       const int leaves = 1 << L.l;
       for (int i = 0; i < leaves; ++i) {
-        u64 w[2];
+        u64 w[KEY_WORDS];
         key_to_words<Key>(tr[i], w);
         if (info->tree) key_to_raw<DT>(w, (unsigned char *)info->tree + (size_t)i * cap->key_bytes);
         key_to_words<Key>(tr[KI + i], w);
@@ -666,6 +677,7 @@ static int dtype_bytes(int dtype) {
     case DT_PAIR: return 16;
     case DT_REC100: return 100;
     case DT_U32: return 4;
+    case DT_QUARTET: return 32;
     default: return 0;
   }
 }
@@ -765,6 +777,7 @@ int ips4o_sort_ex(void *ptr, uint64_t n, int dtype, void *stream, const ips4o_op
     case DT_PAIR: rc = sort_impl<DT_PAIR>(c, base, n, nullptr); break;
     case DT_REC100: rc = sort_impl<DT_REC100>(c, base, n, nullptr); break;
     case DT_U32: rc = sort_impl<DT_U32>(c, base, n, nullptr); break;
+    case DT_QUARTET: rc = sort_impl<DT_QUARTET>(c, base, n, nullptr); break;
   }
   finish_ctx(c, rc);
   return rc;
@@ -857,6 +870,7 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
     case DT_F64: B = Traits<DT_F64>::B; KI = Traits<DT_F64>::KIDX; M = Traits<DT_F64>::BASE_CAP; break;
     case DT_PAIR: B = Traits<DT_PAIR>::B; KI = Traits<DT_PAIR>::KIDX; M = Traits<DT_PAIR>::BASE_CAP; break;
     case DT_U32: B = Traits<DT_U32>::B; KI = Traits<DT_U32>::KIDX; M = Traits<DT_U32>::BASE_CAP; break;
+    case DT_QUARTET: B = Traits<DT_QUARTET>::B; KI = Traits<DT_QUARTET>::KIDX; M = Traits<DT_QUARTET>::BASE_CAP; keyb = 24; break;
     default: B = Traits<DT_REC100>::B; KI = Traits<DT_REC100>::KIDX; M = Traits<DT_REC100>::BASE_CAP; keyb = 16; break;
   }
   if (opt && opt->base_cap > 0 && (u64)opt->base_cap < M) M = (u64)opt->base_cap;
@@ -915,13 +929,14 @@ int ips4o_get_dtype_info(int dtype, ips4o_dtype_info *out) {
   out->block_elems = Traits<DTc>::B;              \
   out->kidx_max = Traits<DTc>::KIDX;              \
   out->base_cap = Traits<DTc>::BASE_CAP;          \
-  out->key_bytes = DTc == DT_REC100 ? 16 : DTc == DT_U32 ? 4 : 8; \
+  out->key_bytes = DTc == DT_REC100 ? 16 : DTc == DT_U32 ? 4 : DTc == DT_QUARTET ? 24 : 8; \
   return IPS4O_OK;
     case DT_U64: FILL(DT_U64)
     case DT_F64: FILL(DT_F64)
     case DT_PAIR: FILL(DT_PAIR)
     case DT_REC100: FILL(DT_REC100)
     case DT_U32: FILL(DT_U32)
+    case DT_QUARTET: FILL(DT_QUARTET)
 #undef FILL
     default: return IPS4O_ERR_INVALID;
   }
@@ -935,7 +950,7 @@ int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream, const i
   Ctx c;
   int rc = init_ctx(c, stream, opt, nullptr);
   if (rc) return rc;
-  StepCapture cap{info, dtype == DT_REC100 ? 16 : dtype == DT_U32 ? 4 : 8};
+  StepCapture cap{info, dtype == DT_REC100 ? 16 : dtype == DT_U32 ? 4 : dtype == DT_QUARTET ? 24 : 8};
   char *base = reinterpret_cast<char *>(ptr);
   switch (dtype) {
     case DT_U64: rc = sort_impl<DT_U64>(c, base, n, &cap); break;
@@ -943,6 +958,7 @@ int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream, const i
     case DT_PAIR: rc = sort_impl<DT_PAIR>(c, base, n, &cap); break;
     case DT_REC100: rc = sort_impl<DT_REC100>(c, base, n, &cap); break;
     case DT_U32: rc = sort_impl<DT_U32>(c, base, n, &cap); break;
+    case DT_QUARTET: rc = sort_impl<DT_QUARTET>(c, base, n, &cap); break;
   }
   if (rc == 0) {
     cudaError_t e = cudaStreamSynchronize(c.st);
@@ -959,7 +975,7 @@ template <int DT>
 static int classify_impl(const void *elems, u64 n, const unsigned char *raw, int u, int eq, u32 *out,
                          cudaStream_t st) {
   using Key = typename Traits<DT>::Key;
-  const int kb = DT == DT_REC100 ? 16 : DT == DT_U32 ? 4 : 8;
+  const int kb = DT == DT_REC100 ? 16 : DT == DT_U32 ? 4 : DT == DT_QUARTET ? 24 : 8;
   int leaves = 1;
   while (leaves < u + 1) leaves <<= 1;
   if (leaves > 256) return IPS4O_ERR_INVALID;
@@ -967,7 +983,7 @@ static int classify_impl(const void *elems, u64 n, const unsigned char *raw, int
   while ((1 << l) < leaves) ++l;
   std::vector<Key> keys(u), tree(leaves), spl(leaves);
   for (int i = 0; i < u; ++i) {
-    u64 w[2];
+    u64 w[KEY_WORDS];
     raw_to_key<DT>(raw + (size_t)i * kb, w);
     keys[i] = key_from_words<Key>(w);
   }
@@ -1007,6 +1023,7 @@ extern "C" int ips4o_classify(const void *elems, uint64_t n, int dtype, const vo
     case DT_F64: return classify_impl<DT_F64>(elems, n, raw, u, equality, out, st);
     case DT_PAIR: return classify_impl<DT_PAIR>(elems, n, raw, u, equality, out, st);
     case DT_U32: return classify_impl<DT_U32>(elems, n, raw, u, equality, out, st);
+    case DT_QUARTET: return classify_impl<DT_QUARTET>(elems, n, raw, u, equality, out, st);
     default: return classify_impl<DT_REC100>(elems, n, raw, u, equality, out, st);
   }
 }

@@ -47,6 +47,18 @@ template <> struct BaseItem<DT_U32> {
   __device__ static Key key(const Item &it) { return it; }
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
 };
+struct alignas(16) QuartetItem {
+  u64 a, b, c, v;
+};
+template <> struct BaseItem<DT_QUARTET> {
+  using Item = QuartetItem;
+  using Key = K192;
+  static constexpr int THREADS = 512, DBMAX = 13, CAP = Traits<DT_QUARTET>::BASE_CAP;
+  static constexpr bool STAGE_RECORDS = false, KEY_ONLY = false;
+  __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const QuartetItem *>(e); }
+  __device__ static Key key(const Item &it) { return K192(it.c, it.b, it.a); }
+  __device__ static bool less(const Item &x, const Item &y) { return key(x) < key(y); }
+};
 struct alignas(16) PairItem {
   u64 key, val;
 };
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         }
       }
       const int pos = a + rank;
-      if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32) {
+      if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
         reinterpret_cast<Item *>(g)[pos] = it;
       } else if constexpr (DT == DT_F64) {
         reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);

@@ -13,7 +13,7 @@ constexpr int PRE_UNROLL = 4;
 
 struct PrepassPart {
   u32 nd, ni, pad0, pad1;
-  u64 mn[2], mx[2];
+  u64 mn[KEY_WORDS], mx[KEY_WORDS];
 };
 
 template <class Key>
@@ -26,9 +26,19 @@ __device__ __forceinline__ u128 shfl_key<u128>(u128 v, int src) {
   u64 hi = __shfl_sync(0xffffffffu, (u64)(v >> 64), src);
   return ((u128)hi << 64) | lo;
 }
+template <>
+__device__ __forceinline__ K192 shfl_key<K192>(K192 v, int src) {
+  return K192(__shfl_sync(0xffffffffu, v.w[0], src), __shfl_sync(0xffffffffu, v.w[1], src),
+              __shfl_sync(0xffffffffu, v.w[2], src));
+}
 template <class Key>
 __device__ __forceinline__ Key shfl_xor_key(Key v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
+}
+template <>
+__device__ __forceinline__ K192 shfl_xor_key<K192>(K192 v, int m) {
+  return K192(__shfl_xor_sync(0xffffffffu, v.w[0], m), __shfl_xor_sync(0xffffffffu, v.w[1], m),
+              __shfl_xor_sync(0xffffffffu, v.w[2], m));
 }
 template <>
 __device__ __forceinline__ u128 shfl_xor_key<u128>(u128 v, int m) {

@@ -254,6 +254,14 @@ template <> __device__ __forceinline__ uint4 ld_cg_unit<uint4>(const uint4 *p) {
   return v;
 }
 
+template <class Unit> __device__ __forceinline__ Unit shfl_unit(const Unit &u, int src) {
+  return __shfl_sync(0xffffffffu, u, src);
+}
+template <> __device__ __forceinline__ uint4 shfl_unit<uint4>(const uint4 &u, int src) {
+  return make_uint4(__shfl_sync(0xffffffffu, u.x, src), __shfl_sync(0xffffffffu, u.y, src),
+                    __shfl_sync(0xffffffffu, u.z, src), __shfl_sync(0xffffffffu, u.w, src));
+}
+
 template <class Unit> __device__ __forceinline__ u32 fold32(const Unit &u);
 template <> __device__ __forceinline__ u32 fold32<u64>(const u64 &u) { return (u32)u ^ (u32)(u >> 32); }
 template <> __device__ __forceinline__ u32 fold32<u32>(const u32 &u) { return u; }
@@ -364,7 +372,7 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
         ku[0] = r[0];
       } else {
 #pragma unroll
-        for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = __shfl_sync(0xffffffffu, r[0], q);
+        for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = shfl_unit(r[0], q);
       }
       u32 b = 0;
       if (lane == 0) {

@@ -8,7 +8,7 @@ namespace ips4o {
 
 constexpr int SAMPLE_THREADS = 1024;  // = SORT_THREADS
 // at most 16 keys per thread of the register sort (4 for 16-byte keys)
-template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D == 100 ? 4096 : 16384; }
+template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D >= 32 ? 4096 : 16384; }
 // dynamic shared memory of sample_kernel: p sample slots + 16-bit digit
 // counters (sized per launch, so levels of small tasks run 2 CTAs per SM)
 template <int DT> __host__ __device__ constexpr size_t sample_smem(size_t p = (size_t)sample_max<DT>()) {
@@ -36,7 +36,10 @@ constexpr int SORT_THREADS = 1024;
 
 template <class Key>
 __device__ __forceinline__ Key shfl_xor_k(Key v, int m) {
-  if constexpr (sizeof(Key) == 8) {
+  if constexpr (sizeof(Key) == sizeof(K192)) {
+    return Key(__shfl_xor_sync(0xffffffffu, v.w[0], m), __shfl_xor_sync(0xffffffffu, v.w[1], m),
+               __shfl_xor_sync(0xffffffffu, v.w[2], m));
+  } else if constexpr (sizeof(Key) == 8) {
     return __shfl_xor_sync(0xffffffffu, v, m);
   } else {
     u64 lo = __shfl_xor_sync(0xffffffffu, (u64)v, m);

@@ -178,6 +178,21 @@ def pairs(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def quartets(n: int, seed: int) -> np.ndarray:
+    """(n, 4) uint64 Quartet elements {a, b, c, value=i}.  a takes
+    only 2^12 values and b 2^20, so the lexicographic order is decided by b
+    and by c often (Alg. 3)."""
+    out = np.empty((n, 4), dtype=np.uint64)
+    for c0 in range(0, n, CHUNK):
+        c1 = min(n, c0 + CHUNK)
+        w = splitmix(seed, 3 * c0, 3 * (c1 - c0)).reshape(c1 - c0, 3)
+        out[c0:c1, 0] = w[:, 0] >> np.uint64(52)
+        out[c0:c1, 1] = w[:, 1] >> np.uint64(44)
+        out[c0:c1, 2] = w[:, 2]
+        out[c0:c1, 3] = np.arange(c0, c1, dtype=np.uint64)
+    return out
+
+
 def records100(n: int, seed: int) -> np.ndarray:
     """(n, 100) uint8 records; key = bytes 0..9."""
     out = np.empty((n, 100), dtype=np.uint8)
@@ -204,6 +219,7 @@ DISTRIBUTIONS = {
     "zero_u64": ("u64", zero_u64),
     "eightdup_u64": ("u64", eightdup_u64),
     "uniform_u32": ("u32", uniform_u32),
+    "quartets": ("quartet", quartets),
     "pairs": ("pair", pairs),
     "records100": ("rec100", records100),
 }

@@ -1,10 +1,10 @@
 """Helpers for the GPU tests: move numpy arrays through the C ABI and back."""
 import numpy as np
 
-U64, F64, PAIR, REC100, U32 = 0, 1, 2, 3, 4
-NAMES = {U64: "u64", F64: "f64", PAIR: "pair", REC100: "rec100", U32: "u32"}
-ELEM = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4}
-KEYB = {U64: 8, F64: 8, PAIR: 8, REC100: 16, U32: 4}
+U64, F64, PAIR, REC100, U32, QUARTET = 0, 1, 2, 3, 4, 5
+NAMES = {U64: "u64", F64: "f64", PAIR: "pair", REC100: "rec100", U32: "u32", QUARTET: "quartet"}
+ELEM = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}
+KEYB = {U64: 8, F64: 8, PAIR: 8, REC100: 16, U32: 4, QUARTET: 24}
 
 
 def to_dev(a: np.ndarray):

@@ -21,7 +21,7 @@ import numpy as np
 import pytest
 
 import synth_inputs as gen
-from gpu_util import F64, PAIR, REC100, U32, U64
+from gpu_util import F64, PAIR, QUARTET, REC100, U32, U64
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -182,6 +182,15 @@ def test_u32_uniform_2p28(ips, orc):
     b = a[: 1 << 22].copy()
     gb = run(ips, b, U32)
     assert orc.parity(gb, orc.sort(b, U32), U32) == -1
+
+
+def test_quartet_2p24_full_oracle(ips, orc):
+    """Quartet (Alg. 3) at 2^24 (512 MiB) against the
+    full oracle: identical key sequence and record multisets."""
+    n = 1 << 24
+    a = gen.quartets(n, 7)
+    g = run(ips, a, QUARTET)
+    assert orc.parity(g, orc.sort(a, QUARTET), QUARTET) == -1
 
 
 def test_c4_pairs(ips, orc):

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import synth_inputs as gen
-from gpu_util import (F64, PAIR, REC100, U32, U64, from_dev, gpu_sort, key_bytes_of,
+from gpu_util import (F64, PAIR, QUARTET, REC100, U32, U64, from_dev, gpu_sort, key_bytes_of,
                       splitters_as_elements, to_dev)
 
 pytestmark = pytest.mark.gpu
@@ -35,6 +35,16 @@ def ips():
 
 def make(dtype, n, seed, kind="uniform"):
     rng = np.random.default_rng(seed)
+    if dtype == QUARTET:
+        q = gen.quartets(n, seed)
+        if kind == "dups":
+            q[:, 0] = rng.integers(0, 2, n).astype(np.uint64)
+            q[:, 1] = rng.integers(0, 3, n).astype(np.uint64)
+            q[:, 2] = rng.integers(0, max(2, n // 16), n).astype(np.uint64)
+        if kind == "few":
+            q[:, :3] = 0
+            q[:, 2] = rng.integers(0, 3, n).astype(np.uint64)
+        return q
     if dtype == U32:
         if kind == "uniform":
             return gen.uniform_u32(n, seed)
@@ -81,7 +91,7 @@ def check(orc, a, g, dtype):
 
 
 # ----------------------------------------------------------------- classifier
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("eq", [False, True])
 def test_device_classifier_matches_oracle(ips, orc, dtype, eq):
     """The tree_bucket used by the classification/permutation kernels equals the
@@ -112,7 +122,7 @@ def test_device_classifier_matches_oracle(ips, orc, dtype, eq):
 
 
 # ----------------------------------------------------------------- one level
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("n,kind", [(5003, "uniform"), (100003, "uniform"), (70001, "dups"),
                                     (40000, "few"), (1 << 20, "uniform")])
 def test_partition_step_tree(ips, orc, dtype, n, kind):
@@ -161,7 +171,7 @@ def test_partition_step_tree(ips, orc, dtype, n, kind):
         assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1, j
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("n", [5003, 300007])
 def test_partition_step_digit(ips, orc, dtype, n):
     """IPS2Ra step: bucket j holds exactly the elements whose
@@ -189,7 +199,7 @@ def test_partition_step_digit(ips, orc, dtype, n):
 SIZES = [0, 1, 2, 3, 31, 32, 33, 63, 64, 65, 4095, 4097, 24575, 24576, 24577, 49153, 100003]
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("n", SIZES)
 def test_sort_sizes(ips, orc, dtype, n):
     a = make(dtype, n, n + 1, "uniform")
@@ -197,7 +207,7 @@ def test_sort_sizes(ips, orc, dtype, n):
     check(orc, a, g, dtype)
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("kind", ["uniform", "dups", "few"])
 @pytest.mark.parametrize("base_cap", [300, 1024])
 def test_sort_deep_recursion(ips, orc, dtype, kind, base_cap):
@@ -210,7 +220,7 @@ def test_sort_deep_recursion(ips, orc, dtype, kind, base_cap):
         assert st["levels"] >= 2
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("kind", ["uniform", "dups", "few"])
 def test_sort_digit_algo(ips, orc, dtype, kind):
     n = 200003 if dtype != REC100 else 50001

@@ -18,7 +18,7 @@ import pytest
 import synth_inputs as gen
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-U64, F64, PAIR, REC100, U32 = 0, 1, 2, 3, 4
+U64, F64, PAIR, REC100, U32, QUARTET = 0, 1, 2, 3, 4, 5
 
 
 # ----------------------------------------------------------------- helpers
@@ -28,6 +28,8 @@ def py_key(dtype, rec: bytes):
         return struct.unpack("<Q", rec)[0]
     if dtype == U32:
         return struct.unpack("<I", rec)[0]
+    if dtype == QUARTET:
+        return struct.unpack("<QQQ", rec[:24])  # Alg. 3: a, then b, then c
     if dtype == F64:
         return struct.unpack("<d", rec)[0]
     if dtype == PAIR:
@@ -36,7 +38,7 @@ def py_key(dtype, rec: bytes):
 
 
 def to_records(arr, dtype):
-    D = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4}[dtype]
+    D = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}[dtype]
     b = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
     return [bytes(b[i * D:(i + 1) * D]) for i in range(b.size // D)]
 
@@ -60,6 +62,14 @@ def battery(dtype, rng):
             cases.append([np.uint64(n - i) for i in range(n)])
             cases.append([np.uint64(i % 5) for i in range(n)])
             cases.append([np.uint64(0 if i % 3 else 2**64 - 1) for i in range(n)])
+        elif dtype == QUARTET:
+            # (a, b, c) triples with many ties in a and in (a, b)
+            cases.append([(int(rng.integers(0, 3)), int(rng.integers(0, 3)), int(rng.integers(0, 2**64, dtype=np.uint64)))
+                          for _ in range(n)])
+            cases.append([(7, 7, 7)] * n)
+            cases.append([(i % 2, (i // 2) % 2, i % 3) for i in range(n)])
+            cases.append([(0, 0, n - i) for i in range(n)])
+            cases.append([(2**64 - 1 if i % 2 else 0, i % 3, 2**64 - 1 - i) for i in range(n)])
         elif dtype == U32:
             cases.append([int(x) for x in rng.integers(0, 2**32, n, dtype=np.uint64)])
             cases.append([7] * n)
@@ -101,6 +111,12 @@ def case_to_array(case, dtype, rng):
         return np.array(case, dtype=np.uint64)
     if dtype == U32:
         return np.array(case, dtype=np.uint32)
+    if dtype == QUARTET:
+        a = np.zeros((len(case), 4), dtype=np.uint64)
+        for i, (x, y, z) in enumerate(case):
+            a[i, :3] = (x, y, z)
+        a[:, 3] = rng.integers(0, 2**64, len(case), dtype=np.uint64)
+        return a
     if dtype == F64:
         return np.array(case, dtype=np.float64)
     if dtype == PAIR:
@@ -113,7 +129,7 @@ def case_to_array(case, dtype, rng):
 
 
 # ----------------------------------------------------------------- mergesort vs brute force
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 def test_mergesort_matches_brute_force_and_python_sorted(orc, dtype):
     """output = input in sorted order.  Stable mergesort, stable
     insertion sort and stable Python sorted() must agree byte for byte."""
@@ -130,18 +146,21 @@ def test_mergesort_matches_brute_force_and_python_sorted(orc, dtype):
         assert orc.multiset_hash(m, dtype) == orc.multiset_hash(a, dtype)
 
 
-@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32])
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 def test_mergesort_all_sequences_over_three_values(orc, dtype):
     """every permutation of every multiset of size <= 7
     over <= 3 distinct values (= all sequences over {v0,v1,v2})."""
     vals = {U64: [0, 1, 2**63 + 5], F64: [-2.0, 0.0, 3.5], PAIR: [0, 1, 2**63 + 5],
-            REC100: [0, 1, 255], U32: [0, 1, 2**31 + 5]}[dtype]
+            REC100: [0, 1, 255], U32: [0, 1, 2**31 + 5], QUARTET: [0, 1, 2]}[dtype]
     for n in range(0, 8):
         for seq in itertools.product(range(3), repeat=n):
             if dtype == U64:
                 a = np.array([vals[s] for s in seq], dtype=np.uint64)
             elif dtype == U32:
                 a = np.array([vals[s] for s in seq], dtype=np.uint32)
+            elif dtype == QUARTET:
+                # the order lives in c while a and b tie, payload tags in value
+                a = np.array([[5, 9, vals[s], i] for i, s in enumerate(seq)], dtype=np.uint64).reshape(-1, 4)
             elif dtype == F64:
                 a = np.array([vals[s] for s in seq], dtype=np.float64)
             elif dtype == PAIR:
@@ -378,6 +397,17 @@ def test_select_splitters_equality_budget(orc):
     assert 2 * leaves <= 256
     sp2, eq2, kf2 = orc.select_splitters(np.arange(m, dtype=np.uint64), 256, 256, U64)
     assert kf2 == 256 and not eq2 and sp2.size // 8 == 255
+
+
+def test_radix_digit_quartet(orc):
+    """IPS2Ra digit of the 192-bit Quartet key a*2^128 + b*2^64 + c (Alg. 3
+    order): compared with Python integers."""
+    rng = np.random.default_rng(6)
+    for _ in range(200):
+        e = rng.integers(0, 2**64, 4, dtype=np.uint64)
+        big = (int(e[0]) << 128) | (int(e[1]) << 64) | int(e[2])
+        for sh, bits in [(0, 8), (60, 8), (120, 8), (184, 8), (127, 3)]:
+            assert orc.radix_digit(QUARTET, e, sh, bits) == (big >> sh) & ((1 << bits) - 1)
 
 
 def test_radix_digit_u32(orc):

@@ -24,8 +24,9 @@ INPUTS = [  # (config, distribution, log2 n, seed)
     ("c5", "records100", 24, 5),
     ("head", "uniform_u64", 30, 42),
     ("next2", "uniform_u32", 30, 6), ("next2", "eightdup_u64", 30, 3), ("next2", "zero_u64", 30, 3),
+    ("next2", "quartets", 26, 7),
 ]
-DT = {"pairs": 2, "records100": 3}
+DT = {"pairs": 2, "records100": 3, "quartets": 5}
 
 
 def main():

@@ -27,7 +27,7 @@ def main():
     import paper_2009_13569_b200 as ips
     import synth_inputs as gen
 
-    dt = {"pairs": 2, "records100": 3}.get(a.dist, 1 if a.dist.endswith("_f64") else 4 if a.dist.endswith("_u32") else 0)
+    dt = {"pairs": 2, "records100": 3, "quartets": 5}.get(a.dist, 1 if a.dist.endswith("_f64") else 4 if a.dist.endswith("_u32") else 0)
     host = np.ascontiguousarray(gen.generate(a.dist, a.nexact or (1 << a.n), 42)).view(np.uint8).reshape(-1)
     src = torch.from_numpy(host).cuda()
     work = torch.empty_like(src)
