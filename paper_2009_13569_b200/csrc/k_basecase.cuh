@@ -190,6 +190,39 @@ __device__ void warp_sort_run(typename BI::Item *a, int n, int lane) {
   warp_bitonic_run<BI>(a, n, lane);
 }
 
+// Whole-bucket fallback: when the digit leaves more than a quarter of the
+// bucket in long runs (keys clustered far below the digit's resolution), the
+// CTA sorts all m items with one bitonic network (flip form, comparators that
+// touch the virtual padding up to the next power of two are skipped).
+template <class BI, int NT>
+__device__ void block_bitonic(typename BI::Item *a, int n) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int q = threadIdx.x; q < P / 2; q += NT) {
+        int i, p;
+        const int blk = q / j, off = q % j;
+        if (j == (k >> 1)) {
+          i = blk * k + off;
+          p = blk * k + (k - 1 - off);
+        } else {
+          i = blk * 2 * j + off;
+          p = i + j;
+        }
+        if (p < n) {
+          const typename BI::Item x = a[i], y = a[p];
+          if (BI::less(y, x)) {
+            a[i] = y;
+            a[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 #ifdef IPS4O_PHASE_TIMING
 #define BC_PHASE(k)                                 \
   if (tid == 0) {                                   \
@@ -217,7 +250,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 *s_hist = reinterpret_cast<u32 *>(smem + S::off_hist);
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
-  __shared__ u32 s_nbig;
+  __shared__ u32 s_nbig, s_bigsum;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
@@ -261,7 +294,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     };
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
     for (int w = tid; w < (1 << BI::DBMAX) / 8; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) s_nbig = 0;
+    if (tid == 0) {
+      s_nbig = 0;
+      s_bigsum = 0;
+    }
     if constexpr (BI::STAGE_RECORDS) {
       // stage the records (coalesced u32 copy)
       const u32 *src = reinterpret_cast<const u32 *>(g);
@@ -325,10 +361,12 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
           if (c0 > RANKMAX) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w;
+            atomicAdd(&s_bigsum, c0);
           }
           if (c1 > RANKMAX) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
+            atomicAdd(&s_bigsum, c1);
           }
         }
         h[q] = st | ((st + c0) << 16);
@@ -368,9 +406,25 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     __syncthreads();
     BC_PHASE(3)
     const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // run ends
-    // 4. long runs: warp bitonic sort in place.  The list holds BIGCAP
-    //    entries; if there are more (a skewed bucket), warps scan the digits.
-    if (!exact) {
+    // 4. long runs: warp sort in place (warp_sort_run).  The list holds
+    //    BIGCAP entries; if there are more (a skewed bucket), warps scan the
+    //    digits.  Mostly long runs of records or pairs (keys clustered far
+    //    below the digit's resolution): the whole bucket is sorted at once.
+    // (key-only items keep the per-run path: its all-equal / few-keys cases
+    // are what long runs of duplicate-heavy inputs are made of)
+    const bool whole = !BI::KEY_ONLY && !exact && s_bigsum > (u32)(m / 4);
+#ifdef IPS4O_BC_DEBUG
+    if (tid == 0 && blockIdx.x < 2 && ti < 4 * gridDim.x) {
+      u64 lw[3], hw[3];
+      key_to_words<Key>(lo, lw);
+      key_to_words<Key>(hi, hw);
+      printf("bc task %u m %d lo %llx:%llx:%llx hi %llx:%llx:%llx bits %d ds %d r32 %u dmul %u nd %d nbig %u bigsum %u whole %d\n",
+             ti, m, lw[2], lw[1], lw[0], hw[2], hw[1], hw[0], bits, ds, r32, dmul, nd, s_nbig, s_bigsum, (int)whole);
+    }
+#endif
+    if (whole) {
+      block_bitonic<BI, NT>(s_items, m);
+    } else if (!exact) {
       const int nbig = (int)s_nbig;
       if (nbig <= BIGCAP) {
         for (int q = wid; q < nbig; q += NT / 32) {
@@ -396,7 +450,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       const int a = d ? (int)s_end[d - 1] : 0;
       const int b = (int)s_end[d];
       int rank = i - a;
-      if (!exact && b - a > 1 && b - a <= RANKMAX) {
+      if (!exact && !whole && b - a > 1 && b - a <= RANKMAX) {
         rank = 0;
         for (int j = a; j < b; ++j) {
           const Item y = s_items[j];
