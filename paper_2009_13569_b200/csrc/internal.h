@@ -92,10 +92,14 @@ struct LevelArgs {
   // scheduler outputs
   TaskDesc *next_tasks;       // next level
   TaskDesc *base_tasks;       // base-case tasks of this level
-  u32 *counters;              // [0] next count, [1] base count, [2] equal elems lo, [3] hi
+  TaskDesc *split_tasks;      // base-case tasks of M < size <= 2M (split in two passes)
+  u32 *counters;              // [0] next count, [1] base count, [2] equal elems lo, [3] hi,
+                              // [4] cleanup invariant violations, [6..7] base elems, [8] split count
   u32 next_cap;
   u32 base_cap_tasks;
   u64 base_cap_elems;         // base-case capacity M (elements)
+  u64 base_split_elems;       // buckets up to this size go to the base case (2M when it can split)
+  char *bc_scratch;           // K7 split scratch: [grid][M] items
   u64 seed;
   u32 dbg_one_agent;          // debug: a single permutation agent per task
   u32 sample_p;               // K1 shared layout: sample slots (pow2 >= every task's m)

@@ -152,6 +152,8 @@ struct LevelPlan {
   u64 nblk = 0;     // block slots (read-done flags)
   u64 child_cap = 0;
   u64 N = 0;
+  u32 bc_grid = 0;   // base-case CTAs
+  u64 bc_cap = 0;    // base-case capacity in use
 };
 
 template <int DT>
@@ -181,8 +183,11 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.rdone = ar.take<unsigned char>(P.nblk);
   A.task_done = ar.take<u32>(T);
   A.minmax = ar.take<u64>(2);
+  A.bc_scratch = BaseItem<DT>::SPLIT ? ar.take<char>((size_t)P.bc_grid * P.bc_cap * sizeof(typename BaseItem<DT>::Item))
+                                     : nullptr;
   A.next_tasks = ar.take<TaskDesc>(P.child_cap);
   A.base_tasks = ar.take<TaskDesc>(P.child_cap);
+  A.split_tasks = BaseItem<DT>::SPLIT ? ar.take<TaskDesc>(P.child_cap) : nullptr;
   A.ntasks = (u32)T;
   A.nstripes = (u32)S;
   A.nperm = (u32)NP;
@@ -212,7 +217,9 @@ template <int DT, int ALGO> static int set_attrs() {
     CK(cudaFuncSetAttribute(classify_v2_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)ClsV2<DT>::bytes));
   }
-  CK(cudaFuncSetAttribute(basecase_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(basecase_kernel<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)BaseSmem<DT>::bytes));
+  CK(cudaFuncSetAttribute(basecase_kernel<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)BaseSmem<DT>::bytes));
   CK(cudaFuncSetAttribute(sample_kernel<DT, ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)sample_smem<DT>()));
@@ -281,6 +288,8 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
     P.child_cap += L.kidx;
   }
   P.nbk = bo;
+  P.bc_grid = (u32)std::min<u64>(std::max<u64>(P.child_cap, 1), (u64)c.sms);
+  P.bc_cap = M;
   return P;
 }
 
@@ -365,6 +374,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   A.algo = ALGO;
   A.seed = c.seed;
   A.base_cap_elems = c.base_cap;
+  A.base_split_elems = BaseItem<DT>::SPLIT ? 2 * c.base_cap : c.base_cap;
   A.dbg_one_agent = c.dbg_one_agent ? 1 : 0;
   // upload the plan (tasks, stripe->task, perm->task) through pinned staging
   const size_t T = P.lt.size(), S = P.stripe_task.size(), NP = P.perm_task.size();
@@ -459,10 +469,16 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
     CKLAUNCH();
     if ((rc = mark(c, KF_SCHED))) return rc;
     if (!c.skip_basecase) {
-      unsigned g = (unsigned)std::min<u64>(std::max<u64>(P.child_cap, 1), (u64)c.sms);
-      basecase_kernel<DT><<<g, BaseItem<DT>::THREADS, BaseSmem<DT>::bytes, c.st>>>(base, A.base_tasks,
-                                                                                    A.counters + 1,
-                                                                                    A.base_cap_tasks);
+      const unsigned g = P.bc_grid;
+      BaseSplitArgs sp{A.bc_scratch, (u32)c.base_cap, A.next_tasks, A.counters, A.next_cap,
+                       reinterpret_cast<unsigned long long *>(A.counters + 6)};
+      basecase_kernel<DT, false><<<g, BaseItem<DT>::THREADS, BaseSmem<DT>::bytes, c.st>>>(
+          base, A.base_tasks, A.counters + 1, A.base_cap_tasks, sp);
+      if constexpr (BaseItem<DT>::SPLIT) {
+        CKLAUNCH();
+        basecase_kernel<DT, true><<<g, BaseItem<DT>::THREADS, BaseSmem<DT>::bytes, c.st>>>(
+            base, A.split_tasks, A.counters + 8, A.base_cap_tasks, sp);
+      }
       CKLAUNCH();
       if ((rc = mark(c, KF_BASE))) return rc;
     }
@@ -516,7 +532,7 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   const u32 nnext = std::min<u32>(hc[0], A.next_cap);
   const u32 nbase = std::min<u32>(hc[1], A.base_cap_tasks);
   if (c.stats) {
-    c.stats->basecase_tasks += nbase;
+    c.stats->basecase_tasks += nbase + std::min<u32>(hc[8], A.base_cap_tasks);
     c.stats->equal_elems += (u64)hc[2] | ((u64)hc[3] << 32);
   }
   next.resize(nnext);
@@ -575,8 +591,9 @@ static int run_base_single(Ctx &c, char *base, const TaskDesc &t) {
   u32 one = 1;
   memcpy(c.pinned + 256, &one, 4);
   CK(cudaMemcpyAsync(buf, c.pinned, 512, cudaMemcpyHostToDevice, c.st));
-  basecase_kernel<DT><<<1, BaseItem<DT>::THREADS, BaseSmem<DT>::bytes, c.st>>>(
-      base, reinterpret_cast<TaskDesc *>(buf), reinterpret_cast<u32 *>(buf + 256), 1);
+  BaseSplitArgs sp{nullptr, (u32)c.base_cap, nullptr, nullptr, 0, nullptr};  // m <= cap: no split
+  basecase_kernel<DT, false><<<1, BaseItem<DT>::THREADS, BaseSmem<DT>::bytes, c.st>>>(
+      base, reinterpret_cast<TaskDesc *>(buf), reinterpret_cast<u32 *>(buf + 256), 1, sp);
   CKLAUNCH();
   if ((rc = mark(c, KF_BASE))) return rc;
   CK(cudaFreeAsync(buf, c.st));
@@ -907,6 +924,7 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
   add(T * BD);
   add(T * 4);
   add(2 * sum_kidx * sizeof(TaskDesc));
+  add((u64)sms * M * (u64)D);  // base-case split scratch (one capacity per CTA)
   return bytes + 256;
 }
 

@@ -24,6 +24,7 @@ template <> struct BaseItem<DT_U64> {
   using Item = u64;
   using Key = u64;
   static constexpr int THREADS = IPS4O_BC_THREADS, DBMAX = 14, CAP = Traits<DT_U64>::BASE_CAP;
+  static constexpr bool SPLIT = true;   // buckets of up to 2 CAP: two shared-memory passes
   static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u64 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -33,6 +34,7 @@ template <> struct BaseItem<DT_F64> {
   using Item = u64;  // order-preserving key
   using Key = u64;
   static constexpr int THREADS = 1024, DBMAX = 14, CAP = Traits<DT_F64>::BASE_CAP;
+  static constexpr bool SPLIT = true;   // buckets of up to 2 CAP: two shared-memory passes
   static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return f64_to_key(*reinterpret_cast<const u64 *>(e)); }
   __device__ static Key key(const Item &it) { return it; }
@@ -42,6 +44,7 @@ template <> struct BaseItem<DT_U32> {
   using Item = u32;
   using Key = u64;
   static constexpr int THREADS = 1024, DBMAX = 15, CAP = Traits<DT_U32>::BASE_CAP;
+  static constexpr bool SPLIT = true;   // buckets of up to 2 CAP: two shared-memory passes
   static constexpr bool STAGE_RECORDS = false, KEY_ONLY = true;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const u32 *>(e); }
   __device__ static Key key(const Item &it) { return it; }
@@ -54,6 +57,7 @@ template <> struct BaseItem<DT_QUARTET> {
   using Item = QuartetItem;
   using Key = K192;
   static constexpr int THREADS = 512, DBMAX = 13, CAP = Traits<DT_QUARTET>::BASE_CAP;
+  static constexpr bool SPLIT = true;   // buckets of up to 2 CAP: two shared-memory passes
   static constexpr bool STAGE_RECORDS = false, KEY_ONLY = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const QuartetItem *>(e); }
   __device__ static Key key(const Item &it) { return K192(it.c, it.b, it.a); }
@@ -66,6 +70,7 @@ template <> struct BaseItem<DT_PAIR> {
   using Item = PairItem;
   using Key = u64;
   static constexpr int THREADS = 512, DBMAX = 14, CAP = Traits<DT_PAIR>::BASE_CAP;
+  static constexpr bool SPLIT = true;   // buckets of up to 2 CAP: two shared-memory passes
   static constexpr bool STAGE_RECORDS = false, KEY_ONLY = false;
   __device__ static Item load(const char *e, u32) { return *reinterpret_cast<const PairItem *>(e); }
   __device__ static Key key(const Item &it) { return it.key; }
@@ -75,6 +80,7 @@ template <> struct BaseItem<DT_REC100> {
   using Item = u128;  // key80 << 16 | index of the record in the staging area
   using Key = u128;
   static constexpr int THREADS = 512, DBMAX = 11, CAP = Traits<DT_REC100>::BASE_CAP;
+  static constexpr bool SPLIT = false;
   static constexpr bool STAGE_RECORDS = true, KEY_ONLY = false;
   __device__ static Item load(const char *e, u32 idx) { return (Traits<DT_REC100>::key(e) << 16) | (u128)idx; }
   __device__ static Key key(const Item &it) { return it >> 16; }
@@ -223,6 +229,20 @@ __device__ void block_bitonic(typename BI::Item *a, int n) {
   }
 }
 
+// Buckets of cap < m <= 2 cap (cap = the base-case capacity in use): split at
+// the largest digit boundary whose start is <= cap; the CTA stages part B in
+// its own global scratch (cap items) while part A is scattered, then sorts
+// part A and part B one after the other.  A bucket that cannot be split
+// that way (one digit run too long) is handed back to the next level.
+struct BaseSplitArgs {
+  char *scratch;        // [gridDim.x][cap] items
+  u32 cap;              // base-case capacity in use (<= BaseItem::CAP)
+  TaskDesc *next_tasks; // next-level task list (K6's output)
+  u32 *next_count;      // its counter (K6 appended first)
+  u32 next_cap;
+  unsigned long long *base_elems;  // base-case element statistic (K6 counted the bucket)
+};
+
 #ifdef IPS4O_PHASE_TIMING
 #define BC_PHASE(k)                                 \
   if (tid == 0) {                                   \
@@ -234,9 +254,9 @@ __device__ void block_bitonic(typename BI::Item *a, int n) {
 #define BC_PHASE(k)
 #endif
 
-template <int DT>
+template <int DT, bool SPLITK>
 __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
-    basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap) {
+    basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap, BaseSplitArgs sp) {
   using Tr = Traits<DT>;
   using BI = BaseItem<DT>;
   using Item = typename BI::Item;
@@ -250,7 +270,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 *s_hist = reinterpret_cast<u32 *>(smem + S::off_hist);
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
-  __shared__ u32 s_nbig, s_bigsum;
+  __shared__ u32 s_nbig, s_bigsum, s_dsplit, s_scnt;
+  Item *scratch = reinterpret_cast<Item *>(sp.scratch) + (size_t)blockIdx.x * sp.cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
   if (count > count_cap) count = count_cap;
@@ -297,6 +318,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     if (tid == 0) {
       s_nbig = 0;
       s_bigsum = 0;
+      s_dsplit = 0;
+      s_scnt = 0;
     }
     if constexpr (BI::STAGE_RECORDS) {
       // stage the records (coalesced u32 copy)
@@ -384,99 +407,141 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
     __syncthreads();
     BC_PHASE(2)
-    // 3. scatter into shared memory in digit order (the second read of the
-    //    bucket hits L2); afterwards the counters hold the run ENDS
-    for (int i0 = tid; i0 < m; i0 += NT * BU) {
-      Item it[BU];
-#pragma unroll
-      for (int u = 0; u < BU; ++u) {
-        const int i = i0 + u * NT;
-        if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
+    const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // starts, ends after the scatter
+    // split point of an oversized bucket (see BaseSplitArgs)
+    int dsplit = nd, mA = m;
+    if (SPLITK && BI::SPLIT && m > (int)sp.cap) {
+      for (int d = tid; d < nd; d += NT)
+        if ((u32)s_end[d] <= sp.cap) atomicMax(&s_dsplit, (u32)d);
+      __syncthreads();
+      dsplit = (int)s_dsplit;
+      mA = (int)s_end[dsplit];
+      if (m - mA > (int)sp.cap || mA == 0) {
+        // no digit boundary leaves both parts within the capacity: the
+        // bucket goes to the next partitioning level instead
+        if (tid == 0) {
+          const u32 slot = atomicAdd(sp.next_count, 1u);
+          if (slot < sp.next_cap) sp.next_tasks[slot] = t;
+          atomicAdd(sp.base_elems, (unsigned long long)(-(long long)m));
+        }
+        __syncthreads();
+        continue;
       }
+    }
+    const int npass = SPLITK && dsplit < nd ? 2 : 1;
+    for (int pass = 0; pass < npass; ++pass) {
+      const int off = pass ? mA : 0;           // global position of s_items[0]
+      const int mp = pass ? m - mA : mA;       // items of this pass
+      const int dlo = pass ? dsplit : 0, dhi = pass ? nd : dsplit;
+      // 3. scatter into shared memory in digit order (pass 0 reads the bucket
+      //    again, from L2; items of part B go to the scratch); afterwards the
+      //    counters of the pass's digits hold the run ENDS
+      if (pass == 0) {
+        for (int i0 = tid; i0 < m; i0 += NT * BU) {
+          Item it[BU];
 #pragma unroll
-      for (int u = 0; u < BU; ++u) {
-        if (i0 + u * NT < m) {
-          const u32 d = digit(it[u]);
+          for (int u = 0; u < BU; ++u) {
+            const int i = i0 + u * NT;
+            if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
+          }
+#pragma unroll
+          for (int u = 0; u < BU; ++u) {
+            if (i0 + u * NT < m) {
+              const u32 d = digit(it[u]);
+              if (!SPLITK || (int)d < dsplit) {
+                const int sh = (d & 1) << 4;
+                const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
+                s_items[(old >> sh) & 0xFFFFu] = it[u];
+              } else {
+                scratch[atomicAdd(&s_scnt, 1u)] = it[u];
+              }
+            }
+          }
+        }
+      } else if constexpr (SPLITK) {
+        for (int i = tid; i < mp; i += NT) {
+          const Item it = scratch[i];
+          const u32 d = digit(it);
           const int sh = (d & 1) << 4;
           const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
-          s_items[(old >> sh) & 0xFFFFu] = it[u];
+          s_items[(int)((old >> sh) & 0xFFFFu) - off] = it;
         }
       }
-    }
-    __syncthreads();
-    BC_PHASE(3)
-    const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // run ends
-    // 4. long runs: warp sort in place (warp_sort_run).  The list holds
-    //    BIGCAP entries; if there are more (a skewed bucket), warps scan the
-    //    digits.  Mostly long runs of records or pairs (keys clustered far
-    //    below the digit's resolution): the whole bucket is sorted at once.
-    // (key-only items keep the per-run path: its all-equal / few-keys cases
-    // are what long runs of duplicate-heavy inputs are made of)
-    const bool whole = !BI::KEY_ONLY && !exact && s_bigsum > (u32)(m / 4);
-#ifdef IPS4O_BC_DEBUG
-    if (tid == 0 && blockIdx.x < 2 && ti < 4 * gridDim.x) {
-      u64 lw[3], hw[3];
-      key_to_words<Key>(lo, lw);
-      key_to_words<Key>(hi, hw);
-      printf("bc task %u m %d lo %llx:%llx:%llx hi %llx:%llx:%llx bits %d ds %d r32 %u dmul %u nd %d nbig %u bigsum %u whole %d\n",
-             ti, m, lw[2], lw[1], lw[0], hw[2], hw[1], hw[0], bits, ds, r32, dmul, nd, s_nbig, s_bigsum, (int)whole);
-    }
-#endif
-    if (whole) {
-      block_bitonic<BI, NT>(s_items, m);
-    } else if (!exact) {
-      const int nbig = (int)s_nbig;
-      if (nbig <= BIGCAP) {
-        for (int q = wid; q < nbig; q += NT / 32) {
-          int d = (int)s_big[q];
-          int a = d ? (int)s_end[d - 1] : 0;
-          warp_sort_run<BI>(s_items + a, (int)s_end[d] - a, lane);
-        }
-      } else {
-        for (int d = wid; d < nd; d += NT / 32) {
-          int a = d ? (int)s_end[d - 1] : 0;
-          int n = (int)s_end[d] - a;
-          if (n > RANKMAX) warp_sort_run<BI>(s_items + a, n, lane);
-        }
-      }
-      if (nbig) __syncthreads();
-    }
-    BC_PHASE(4)
-    // 5. rank inside the run by counting (independent compares, so warps keep
-    //    several loads in flight), write to the final position
-    for (int i = tid; i < m; i += NT) {
-      const Item it = s_items[i];
-      const u32 d = digit(it);
-      const int a = d ? (int)s_end[d - 1] : 0;
-      const int b = (int)s_end[d];
-      int rank = i - a;
-      if (!exact && !whole && b - a > 1 && b - a <= RANKMAX) {
-        rank = 0;
-        for (int j = a; j < b; ++j) {
-          const Item y = s_items[j];
-          rank += (BI::less(y, it) || (!BI::less(it, y) && j < i)) ? 1 : 0;
-        }
-      }
-      const int pos = a + rank;
-      if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
-        reinterpret_cast<Item *>(g)[pos] = it;
-      } else if constexpr (DT == DT_F64) {
-        reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
-      } else {
-        s_sidx[pos] = (unsigned short)(it & (Item)0xFFFF);
-      }
-    }
-    if constexpr (BI::STAGE_RECORDS) {
       __syncthreads();
-      // records: warp per record, lanes copy the 25 words
-      u32 *out = reinterpret_cast<u32 *>(g);
-      for (int i = wid; i < m; i += NT / 32) {
-        const u32 *src = reinterpret_cast<const u32 *>(s_rec + (size_t)s_sidx[i] * D);
-        if (lane < D / 4) out[(size_t)i * (D / 4) + lane] = src[lane];
+      BC_PHASE(3)
+      // 4. long runs: warp sort in place (warp_sort_run).  The list holds
+      //    BIGCAP entries; if there are more (a skewed bucket), warps scan the
+      //    digits.  Mostly long runs of records or pairs (keys clustered far
+      //    below the digit's resolution): the whole pass is sorted at once.
+      //    (key-only items keep the per-run path: its all-equal / few-keys
+      //    cases are what long runs of duplicate-heavy inputs are made of)
+      const bool whole = !BI::KEY_ONLY && !exact && s_bigsum > (u32)(m / 4);
+#ifdef IPS4O_BC_DEBUG
+      if (tid == 0 && blockIdx.x < 2 && ti < 4 * gridDim.x) {
+        u64 lw[3], hw[3];
+        key_to_words<Key>(lo, lw);
+        key_to_words<Key>(hi, hw);
+        printf("bc task %u m %d pass %d lo %llx:%llx:%llx hi %llx:%llx:%llx bits %d ds %d nd %d nbig %u bigsum %u whole %d\n",
+               ti, m, pass, lw[2], lw[1], lw[0], hw[2], hw[1], hw[0], bits, ds, nd, s_nbig, s_bigsum, (int)whole);
       }
+#endif
+      if (whole) {
+        block_bitonic<BI, NT>(s_items, mp);
+      } else if (!exact) {
+        const int nbig = (int)s_nbig;
+        if (nbig <= BIGCAP) {
+          for (int q = wid; q < nbig; q += NT / 32) {
+            const int d = (int)s_big[q];
+            if (d < dlo || d >= dhi) continue;
+            const int a = d ? (int)s_end[d - 1] : 0;
+            warp_sort_run<BI>(s_items + (a - off), (int)s_end[d] - a, lane);
+          }
+        } else {
+          for (int d = dlo + wid; d < dhi; d += NT / 32) {
+            const int a = d ? (int)s_end[d - 1] : 0;
+            const int n = (int)s_end[d] - a;
+            if (n > RANKMAX) warp_sort_run<BI>(s_items + (a - off), n, lane);
+          }
+        }
+        if (nbig) __syncthreads();
+      }
+      BC_PHASE(4)
+      // 5. rank inside the run by counting (independent compares, so warps
+      //    keep several loads in flight), write to the final position
+      for (int i = tid; i < mp; i += NT) {
+        const Item it = s_items[i];
+        const u32 d = digit(it);
+        const int a = (d ? (int)s_end[d - 1] : 0) - off;
+        const int b = (int)s_end[d] - off;
+        int rank = i - a;
+        if (!exact && !whole && b - a > 1 && b - a <= RANKMAX) {
+          rank = 0;
+          for (int j = a; j < b; ++j) {
+            const Item y = s_items[j];
+            rank += (BI::less(y, it) || (!BI::less(it, y) && j < i)) ? 1 : 0;
+          }
+        }
+        const int pos = off + a + rank;
+        if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
+          reinterpret_cast<Item *>(g)[pos] = it;
+        } else if constexpr (DT == DT_F64) {
+          reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
+        } else {
+          s_sidx[pos] = (unsigned short)(it & (Item)0xFFFF);
+        }
+      }
+      if constexpr (BI::STAGE_RECORDS) {
+        __syncthreads();
+        // records: warp per record, lanes copy the 25 words
+        u32 *out = reinterpret_cast<u32 *>(g);
+        for (int i = wid; i < m; i += NT / 32) {
+          const u32 *src = reinterpret_cast<const u32 *>(s_rec + (size_t)s_sidx[i] * D);
+          if (lane < D / 4) out[(size_t)i * (D / 4) + lane] = src[lane];
+        }
+      }
+      __syncthreads();
+      BC_PHASE(5)
     }
-    __syncthreads();
-    BC_PHASE(5)
   }
 #ifdef IPS4O_PHASE_TIMING
   if (tid == 0 && blockIdx.x == 0)

@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
       u32 slot = atomicAdd(&A.counters[1], 1u);
       if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;
       atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
+    } else if (sz <= A.base_split_elems) {
+      // up to twice the capacity: the base case's two-pass split (K7s)
+      u32 slot = atomicAdd(&A.counters[8], 1u);
+      if (slot < A.base_cap_tasks) A.split_tasks[slot] = c;
+      atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
     } else {
       u32 slot = atomicAdd(&A.counters[0], 1u);
       if (slot < A.next_cap) A.next_tasks[slot] = c;
