@@ -236,7 +236,9 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
   LevelPlan P;
   const u64 M = c.base_cap;
   for (auto &t : tasks) P.N += t.size;
-  const u64 target_stripes = (u64)c.sms * 4;
+  u64 spm = 6;  // stripes per SM: smaller CTAs shorten the tail of levels of unequal tasks
+  if (const char *e = getenv("IPS4O_STRIPES_PER_SM")) spm = (u64)std::max(1, atoi(e));  // tuning
+  const u64 target_stripes = (u64)c.sms * spm;
   u64 se = round_up(ceil_div(P.N, target_stripes), B);
   se = std::max<u64>(se, round_up((u64)Tr::CLS_TILE * 2, B));
   const int occ = perm_occupancy<DT>();

@@ -11,19 +11,21 @@ namespace ips4o {
 // the exact boundaries E (prefix sum), the block-rounded delimiters
 // d_j = ceil(E_j / b) * b, the full blocks per bucket, and initialises
 // the packed (w, r) words: w_j = d_j / b, r_j = w_j + f_j - 1.
-constexpr int BND_THREADS = 256;
+constexpr int BND_THREADS = 1024;
 
 template <int DT>
 __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
   constexpr int KI = Tr::KIDX, B = Tr::B;
-  static_assert(KI <= BND_THREADS, "one thread per bucket");
+  constexpr int QB = BND_THREADS / KI;  // threads per bucket, each over a share of the stripes
+  static_assert(KI * QB == BND_THREADS, "whole threads per bucket");
   __shared__ u32 ws[BND_THREADS / 32 + 1];
   __shared__ u64 s_E[KI + 1];
+  __shared__ u32 s_pq[QB][KI];
   const u32 ti = blockIdx.x;
   LevelTask &L = A.tasks[ti];
   const int K = (int)L.K;
-  const int j = threadIdx.x;
+  const int j = threadIdx.x % KI, qb = threadIdx.x / KI;
   // prefix of the stripes' full-block counts (for F(x) below)
   u32 carry = 0;
   for (u32 b0 = 0; b0 < L.nstripes; b0 += BND_THREADS) {
@@ -35,42 +37,44 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
     carry += tot;
   }
   // per bucket: total count over the stripes and the exclusive
-  // prefix over the stripes of the partial-buffer fills (cleanup, K5b)
-  u32 c = 0;
+  // prefix over the stripes of the partial-buffer fills (cleanup, K5b);
+  // QB threads per bucket, each over a contiguous share of the stripes
+  const u32 ns = L.nstripes;
+  const u32 s_lo = (u32)(((u64)ns * qb) / QB), s_hi = (u32)(((u64)ns * (qb + 1)) / QB);
+  u32 c = 0, pc = 0;
   if (j < K) {
-    u32 pc = 0;
-    const u32 ns = L.nstripes;
-    u32 s = 0;
-    for (; s + 8 <= ns; s += 8) {
-      u32 cv[8], pv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const u64 slot = L.sbk_off + (u64)(s + q) * L.kidx + j;
-        cv[q] = A.counts[slot];
-        pv[q] = A.pfill[slot];
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        c += cv[q];
-        A.pcum[L.sbk_off + (u64)(s + q) * L.kidx + j] = pc;
-        pc += pv[q];
-      }
-    }
-    for (; s < ns; ++s) {
+    for (u32 s = s_lo; s < s_hi; ++s) {
       const u64 slot = L.sbk_off + (u64)s * L.kidx + j;
       c += A.counts[slot];
-      A.pcum[slot] = pc;
       pc += A.pfill[slot];
     }
-    A.ptot[L.bucket_off + j] = pc;
+    s_pq[qb][j] = pc;
+  }
+  __syncthreads();
+  if (j < K) {
+    u32 run = 0;
+    for (int q = 0; q < qb; ++q) run += s_pq[q][j];
+    for (u32 s = s_lo; s < s_hi; ++s) {
+      const u64 slot = L.sbk_off + (u64)s * L.kidx + j;
+      A.pcum[slot] = run;
+      run += A.pfill[slot];
+    }
+    if (qb == QB - 1) A.ptot[L.bucket_off + j] = run;
+  }
+  __syncthreads();
+  s_pq[qb][j] = j < K ? c : 0u;  // reuse: per-share counts
+  __syncthreads();
+  if (qb == 0) {
+    c = 0;
+    for (int q = 0; q < QB; ++q) c += s_pq[q][j];
   }
   u32 total;
-  u32 pre = block_exclusive_scan<BND_THREADS>(c, ws, &total);
-  if (j < K) s_E[j] = pre;
-  if (j == 0) s_E[K] = L.t.size;
+  u32 pre = block_exclusive_scan<BND_THREADS>(qb == 0 && j < K ? c : 0u, ws, &total);
+  if (qb == 0 && j < K) s_E[j] = pre;
+  if (threadIdx.x == 0) s_E[K] = L.t.size;
   __syncthreads();
   const u64 bo = L.bucket_off;
-  if (j < K) {
+  if (qb == 0 && j < K) {
     // region j = blocks [ceil(E_j/b), ceil(E_{j+1}/b)); fr = full positions in it
     const u64 SB = L.stripe_elems / B;
     const u64 r0 = (s_E[j] + B - 1) / B, r1 = (s_E[j + 1] + B - 1) / B;
@@ -88,7 +92,7 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
     A.wr[(bo + j) * WR_STRIDE] = (r0 << 32) | (u64)(r + (i64)RBIAS);
     A.wr[(bo + j) * WR_STRIDE + 1] = r0 + fr;  // prefix end (formerly full positions)
   }
-  if (j == 0) {
+  if (threadIdx.x == 0) {
     A.E[bo + K] = L.t.size;
     A.ovf_used[ti] = 0xFFFFFFFFu;
   }
