@@ -237,7 +237,7 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
   const u64 M = c.base_cap;
   for (auto &t : tasks) P.N += t.size;
   u64 spm = 6;  // stripes per SM: smaller CTAs shorten the tail of levels of unequal tasks
-  if (const char *e = getenv("IPS4O_STRIPES_PER_SM")) spm = (u64)std::max(1, atoi(e));  // tuning
+  if (const char *e = getenv("IPS4O_STRIPES_PER_SM")) spm = (u64)std::min(8, std::max(1, atoi(e)));  // tuning
   const u64 target_stripes = (u64)c.sms * spm;
   u64 se = round_up(ceil_div(P.N, target_stripes), B);
   se = std::max<u64>(se, round_up((u64)Tr::CLS_TILE * 2, B));
@@ -900,13 +900,13 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
   // Level 1 has one task; at a level >= 2 every task is a bucket larger than
   // M, so T <= n / (M + 1).  kidx_t <= 2 * next_pow2(ceil(2 s_t / M)) gives
   // sum kidx_t <= 8n/M + 4T; stripes per task <= s_t / se + 1 with
-  // se >= n / (4 SMs) gives S <= 4 SMs + T and sum ns_t kidx_t <= 4 SMs KI + sum kidx_t.
+  // se >= n / (8 SMs) gives S <= 8 SMs + T and sum ns_t kidx_t <= 8 SMs KI + sum kidx_t.
   const u64 T = std::max<u64>(1, n / (M + 1));
-  const u64 S = (u64)sms * 4 + T;
+  const u64 S = (u64)sms * 8 + T;  // plan_level: <= 8 stripes per SM (+1 per task)
   const u64 NP = (u64)sms * 16 + T;
   const u64 sum_kidx = std::min<u64>(T * KI, 8 * (n / std::max<u64>(M, 1) + 1) + 4 * T) + KI;
   const u64 NBK = sum_kidx + T;
-  const u64 NSBK = (u64)sms * 4 * KI + sum_kidx;
+  const u64 NSBK = (u64)sms * 8 * KI + sum_kidx;
   const u64 BD = (u64)B * D;
   u64 bytes = 0;
   auto add = [&](u64 b) { bytes += round_up(b, 256); };
