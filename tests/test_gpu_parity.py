@@ -367,3 +367,18 @@ def test_deterministic(ips):
     g1, _ = gpu_sort(a, U64)
     g2, _ = gpu_sort(a, U64)
     assert np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, U32, QUARTET])
+@pytest.mark.parametrize("kind", ["uniform", "dups"])
+def test_split_base_case(ips, orc, dtype, kind):
+    """K7s: with base_cap M = 1000 and 256 buckets of ~1500 elements, most
+    buckets are sorted by the two-pass split base case (M < m <= 2M); any
+    that cannot be split go to a next level.  Parity with the oracle."""
+    n = 256 * 1500 + 7
+    a = make(dtype, n, 33, kind)
+    g, st = gpu_sort(a, dtype, base_cap=1000)
+    check(orc, a, g, dtype)
+    if kind == "uniform":
+        # nearly every bucket fits the split (levels beyond 1 hold few tasks)
+        assert st["levels"] == 1 or sum(st["tasks_per_level"][1:]) < 32, st["tasks_per_level"]
