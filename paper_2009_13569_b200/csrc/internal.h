@@ -19,6 +19,8 @@ enum : u32 {
   TF_NONE = 0,
   TF_MINMAX = 1,  // bounds unknown ([0, max]); K2 computes the key min/max and
                   // K6 uses them for the children (the pre-pass was skipped)
+  TF_MEASURE = 2, // DIGIT: the parent's digit left more than half of it in this
+                  // bucket; K0m measures the exact key range before the digit setup
 };
 
 // A task T[l, r): the subarray [begin, begin+size) of the input, with
@@ -104,6 +106,9 @@ struct LevelArgs {
   u32 dbg_one_agent;          // debug: a single permutation agent per task
   u32 sample_p;               // K1 shared layout: sample slots (pow2 >= every task's m)
   u64 *minmax;                // [0] = min key, [1] = max key of TF_MINMAX tasks (u64 keys)
+  const u32 *measure_part;    // [2 * nmeasure_parts]: task, part | nparts << 16 (K0m)
+  const u32 *measure_task;    // [3 * nmeasure]: task, first part, nparts (K0m)
+  void *measure_out;          // [nmeasure_parts] PrepassPart: per-part key min/max
 };
 
 // The packed per-bucket permutation word: high 32

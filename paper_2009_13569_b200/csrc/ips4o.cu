@@ -145,6 +145,7 @@ struct Arena {
 struct LevelPlan {
   std::vector<LevelTask> lt;
   std::vector<u32> stripe_task, perm_task;
+  std::vector<u32> measure_part, measure_task;  // K0m lists (TF_MEASURE tasks)
   u32 max_stripes_per_task = 1;
   u32 max_m = 0;
   u64 nbk = 0;      // bucket slots
@@ -183,6 +184,9 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.rdone = ar.take<unsigned char>(P.nblk);
   A.task_done = ar.take<u32>(T);
   A.minmax = ar.take<u64>(2);
+  A.measure_part = ar.take<u32>(P.measure_part.size());
+  A.measure_task = ar.take<u32>(P.measure_task.size());
+  A.measure_out = ar.take<PrepassPart>(P.measure_part.size() / 2);
   A.bc_scratch = BaseItem<DT>::SPLIT ? ar.take<char>((size_t)P.bc_grid * P.bc_cap * sizeof(typename BaseItem<DT>::Item))
                                      : nullptr;
   A.next_tasks = ar.take<TaskDesc>(P.child_cap);
@@ -288,6 +292,16 @@ static LevelPlan plan_level(const Ctx &c, const std::vector<TaskDesc> &tasks) {
     L.sbk_off = P.nsbk;
     P.nsbk += ns * L.kidx;
     P.child_cap += L.kidx;
+    if (t.flags & TF_MEASURE) {
+      const u32 np = (u32)std::min<u64>(MEAS_MAXPARTS, std::max<u64>(1, ceil_div(t.size, MEAS_PART_ELEMS)));
+      P.measure_task.push_back((u32)i);
+      P.measure_task.push_back((u32)(P.measure_part.size() / 2));
+      P.measure_task.push_back(np);
+      for (u32 q = 0; q < np; ++q) {
+        P.measure_part.push_back((u32)i);
+        P.measure_part.push_back(q | np << 16);
+      }
+    }
   }
   P.nbk = bo;
   P.bc_grid = (u32)std::min<u64>(std::max<u64>(P.child_cap, 1), (u64)c.sms);
@@ -380,7 +394,8 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   A.dbg_one_agent = c.dbg_one_agent ? 1 : 0;
   // upload the plan (tasks, stripe->task, perm->task) through pinned staging
   const size_t T = P.lt.size(), S = P.stripe_task.size(), NP = P.perm_task.size();
-  const size_t up = T * sizeof(LevelTask) + (S + NP) * 4 + 64;
+  const size_t MPW = P.measure_part.size(), MTW = P.measure_task.size();
+  const size_t up = T * sizeof(LevelTask) + (S + NP + MPW + MTW) * 4 + 64;
   rc = ensure_pinned(c, std::max<size_t>(up, (P.child_cap + 16) * sizeof(TaskDesc) + 4096));
   if (rc) return rc;
   char *hp = c.pinned;
@@ -390,6 +405,13 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CK(cudaMemcpyAsync(A.tasks, hp, T * sizeof(LevelTask), cudaMemcpyHostToDevice, c.st));
   CK(cudaMemcpyAsync((void *)A.stripe_task, hp + T * sizeof(LevelTask), S * 4, cudaMemcpyHostToDevice, c.st));
   CK(cudaMemcpyAsync((void *)A.perm_task, hp + T * sizeof(LevelTask) + S * 4, NP * 4, cudaMemcpyHostToDevice, c.st));
+  if (MTW) {
+    char *mp = hp + T * sizeof(LevelTask) + (S + NP) * 4;
+    memcpy(mp, P.measure_part.data(), MPW * 4);
+    memcpy(mp + MPW * 4, P.measure_task.data(), MTW * 4);
+    CK(cudaMemcpyAsync((void *)A.measure_part, mp, MPW * 4, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync((void *)A.measure_task, mp + MPW * 4, MTW * 4, cudaMemcpyHostToDevice, c.st));
+  }
   CK(cudaMemsetAsync(A.counters, 0, 16 * 4, c.st));
   CK(cudaMemsetAsync(A.rdone, 0, P.nblk, c.st));
   CK(cudaMemsetAsync(A.task_done, 0, T * 4, c.st));
@@ -397,6 +419,15 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   CK(cudaMemsetAsync(A.minmax + 1, 0, 8, c.st));  // max = 0
   c.ms[KF_HOST] += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - h0).count();
 
+  // K0m exact key ranges of the TF_MEASURE tasks (DIGIT, DESIGN R27)
+  if (ALGO == ALGO_DIGIT && MTW) {
+    measure_part_kernel<DT><<<(unsigned)(MPW / 2), MEAS_THREADS, 0, c.st>>>(A);
+    CKLAUNCH();
+    const unsigned nm = (unsigned)(MTW / 3);
+    measure_reduce_kernel<DT><<<(nm + 127) / 128, 128, 0, c.st>>>(A, nm);
+    CKLAUNCH();
+    if ((rc = mark(c, KF_SAMPLE))) return rc;
+  }
   // K1 sampling + tree (or digit setup)
   {
     const u64 sp = next_pow2_u64(std::max<u64>(P.max_m, SORT_THREADS));
@@ -925,7 +956,14 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
   add(NBK * BD);
   add(T * BD);
   add(T * 4);
-  add(2 * sum_kidx * sizeof(TaskDesc));
+  add(n / B + 2 * T);                   // read-done flags
+  add(T * 4);                           // task_done
+  add(16);                              // minmax
+  const u64 MP = T + n / MEAS_PART_ELEMS + 1;  // K0m parts
+  add(MP * 8);
+  add(T * 12);
+  add(MP * sizeof(PrepassPart));
+  add(3 * sum_kidx * sizeof(TaskDesc));  // next, base, split lists
   add((u64)sms * M * (u64)D);  // base-case split scratch (one capacity per CTA)
   return bytes + 256;
 }

@@ -194,6 +194,9 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
     key_to_words<Key>(hi, c.hi);
     c.level = L.t.level + 1;
     c.flags = 0;
+    // DIGIT: a digit that kept most of the task splits bits the keys do not
+    // use (sparse keys); measure the child's exact range first (DESIGN R27)
+    if (ALGO == ALGO_DIGIT && 2 * sz > L.t.size) c.flags = TF_MEASURE;
     if (sz <= A.base_cap_elems) {
       u32 slot = atomicAdd(&A.counters[1], 1u);
       if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;

@@ -205,4 +205,77 @@ __global__ void classify_test_kernel(const char *elems, u64 n, const typename Tr
     out[i] = tree_bucket<Key>(s_tree, s_spl, l, eq, Tr::key(elems + i * Tr::D));
 }
 
+// K0m: exact key range of the TF_MEASURE tasks of a DIGIT level (DESIGN R27;
+// the per-task analogue of IPS2Ra's significant-bit scan).  One
+// CTA per part of a task (parts of ~64K elements, at most MEAS_MAXPARTS), then
+// one thread per task folds the parts into the task's [lo, hi].
+constexpr int MEAS_THREADS = 512;
+constexpr u64 MEAS_PART_ELEMS = 65536;
+constexpr u32 MEAS_MAXPARTS = 296;
+
+template <int DT>
+__global__ void __launch_bounds__(MEAS_THREADS) measure_part_kernel(LevelArgs A) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  constexpr int D = Tr::D;
+  const u32 ti = A.measure_part[2 * blockIdx.x];
+  const u32 pw = A.measure_part[2 * blockIdx.x + 1];
+  const u64 p = pw & 0xFFFFu, np = pw >> 16;
+  const TaskDesc &t = A.tasks[ti].t;
+  const u64 b0 = t.size * p / np, b1 = t.size * (p + 1) / np;
+  const char *src = A.base + t.begin * D;
+  Key mn = key_max<Key>(), mx = (Key)0;
+  for (u64 e = b0 + threadIdx.x; e < b1; e += MEAS_THREADS) {
+    const Key k = Tr::key(src + e * D);
+    mn = k < mn ? k : mn;
+    mx = k > mx ? k : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Key x = shfl_xor_key(mn, o), y = shfl_xor_key(mx, o);
+    mn = x < mn ? x : mn;
+    mx = y > mx ? y : mx;
+  }
+  __shared__ Key s_mn[MEAS_THREADS / 32], s_mx[MEAS_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_mn[wid] = mn;
+    s_mx[wid] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < MEAS_THREADS / 32; ++w) {
+      mn = s_mn[w] < mn ? s_mn[w] : mn;
+      mx = s_mx[w] > mx ? s_mx[w] : mx;
+    }
+    PrepassPart q;
+    q.nd = q.ni = q.pad0 = q.pad1 = 0;
+    key_to_words<Key>(mn, q.mn);
+    key_to_words<Key>(mx, q.mx);
+    reinterpret_cast<PrepassPart *>(A.measure_out)[blockIdx.x] = q;
+  }
+}
+
+template <int DT>
+__global__ void measure_reduce_kernel(LevelArgs A, u32 nmeasure) {
+  using Key = typename Traits<DT>::Key;
+  const u32 f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nmeasure) return;
+  const u32 ti = A.measure_task[3 * f], first = A.measure_task[3 * f + 1], np = A.measure_task[3 * f + 2];
+  const PrepassPart *parts = reinterpret_cast<const PrepassPart *>(A.measure_out) + first;
+  Key mn = key_max<Key>(), mx = (Key)0;
+  for (u32 i = 0; i < np; ++i) {
+    Key a = key_from_words<Key>(parts[i].mn), b = key_from_words<Key>(parts[i].mx);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  TaskDesc &t = A.tasks[ti].t;
+  const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
+  // the measured range lies inside the bounds; clamp anyway (the bounds are the invariant)
+  if (mn < lo) mn = lo;
+  if (mx > hi) mx = hi;
+  key_to_words<Key>(mn, t.lo);
+  key_to_words<Key>(mx, t.hi);
+}
+
 }  // namespace ips4o

@@ -119,8 +119,11 @@ __device__ __forceinline__ void digit_setup(LevelTask &L) {
   int h = bitlen((Key)(lo ^ hi));
   int kb = log2_i((int)L.k_req);
   int bits = h < kb ? h : kb;
+  // a measured all-equal task (K0m, lo == hi) still gets two buckets; its
+  // child is then terminal
+  if (bits < 1) bits = 1;
   L.l = bits;
-  L.shift = h - bits;
+  L.shift = h > bits ? h - bits : 0;
   L.K = 1u << bits;
   L.equality = 0;
   L.k_used = 1u << bits;

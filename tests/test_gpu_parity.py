@@ -229,6 +229,29 @@ def test_sort_digit_algo(ips, orc, dtype, kind):
     check(orc, a, g, dtype)
 
 
+@pytest.mark.parametrize("dtype", [U64, QUARTET])
+def test_digit_sparse_keys_measured(ips, orc, dtype):
+    """IPS2Ra on keys whose used bits are far apart (DESIGN R27): the level
+    after a futile digit measures its exact range, so the recursion depth stays
+    bounded by the used bits, not by the key width."""
+    n = 1 << 20
+    rng = np.random.default_rng(41)
+    if dtype == U64:
+        a = (rng.integers(0, 256, n).astype(np.uint64) << np.uint64(56)) | rng.integers(0, 1 << 20, n).astype(
+            np.uint64
+        )
+    else:
+        a = gen.quartets(n, 41)  # b: 20 bits of 64, c: 64 bits
+        a[:, 0] = rng.integers(0, 256, n).astype(np.uint64)  # a: 8 bits
+    g, st = gpu_sort(a, dtype, algo=ips.DIGIT, base_cap=1024)
+    check(orc, a, g, dtype)
+    # level 1: digit = a (256 tasks of ~4096); level 2: the digit right below a
+    # is all zero (every task lands in one bucket, flagged); level 3 measures
+    # the range of b and splits it.  Without the measurement the zero bits
+    # between a and b would cost one futile level per digit.
+    assert st["levels"] <= 3, st["tasks_per_level"]
+
+
 def _patterns(n, rng):
     m = np.uint64(2**64 - 1)
     u = gen.uniform_u64(n, 77)
