@@ -279,21 +279,34 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   long long ph_[8] = {0}, tprev_ = clock64();
 #endif
 
+  // Task descriptors are double-buffered in shared memory: lanes of warp 0
+  // load the next one (one word each) while the current bucket is sorted and
+  // publish it after the histogram phase, so no iteration waits on them.
+  constexpr int TDW = sizeof(TaskDesc) / 4;
+  static_assert(TDW <= 32 && sizeof(TaskDesc) % 4 == 0, "one word per lane");
+  __shared__ TaskDesc s_task[2];
+  u32 tdw = 0;
   if (blockIdx.x < count) {
-    const TaskDesc t0 = tasks[blockIdx.x];
-    prefetch_l2(base + t0.begin * (u64)D, t0.size * (u64)D, tid, NT);
+    if (tid < TDW) reinterpret_cast<u32 *>(&s_task[0])[tid] = reinterpret_cast<const u32 *>(&tasks[blockIdx.x])[tid];
+    __syncthreads();
+    prefetch_l2(base + s_task[0].begin * (u64)D, s_task[0].size * (u64)D, tid, NT);
   }
-  for (u32 ti = blockIdx.x; ti < count; ti += gridDim.x) {
-    const TaskDesc t = tasks[ti];
+  int cur = 0;
+  for (u32 ti = blockIdx.x; ti < count; ti += gridDim.x, cur ^= 1) {
+    const TaskDesc &t = s_task[cur];  // valid for the whole iteration
+    const bool has_next = ti + gridDim.x < count;
+    if (has_next && tid < TDW) tdw = reinterpret_cast<const u32 *>(&tasks[ti + gridDim.x])[tid];
+    auto publish_next = [&]() {
+      if (has_next && tid < TDW) reinterpret_cast<u32 *>(&s_task[cur ^ 1])[tid] = tdw;
+    };
     const int m = (int)t.size;
     char *g = base + t.begin * (u64)D;
-    // the next bucket of this CTA streams into L2 while this one is sorted
-    if (ti + gridDim.x < count) {
-      const TaskDesc tn = tasks[ti + gridDim.x];
-      prefetch_l2(base + tn.begin * (u64)D, tn.size * (u64)D, tid, NT);
-    }
     const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
-    if (m <= 1 || !(lo < hi)) continue;
+    if (m <= 1 || !(lo < hi)) {
+      publish_next();
+      __syncthreads();
+      continue;
+    }
     // digit(x) = floor(v(x) * dmul / 2^32) with v(x) = the top 32 bits of
     // x - lo over the bucket's range: monotone in x (all the counting sort
     // needs; the runs are finished by key comparisons) and spread evenly over
@@ -349,8 +362,11 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         }
       }
     }
+    publish_next();
     __syncthreads();
     BC_PHASE(1)
+    // the next bucket of this CTA streams into L2 while this one is sorted
+    if (has_next) prefetch_l2(base + s_task[cur ^ 1].begin * (u64)D, s_task[cur ^ 1].size * (u64)D, tid, NT);
     // 2. exclusive scan in place: thread t owns the WPT consecutive words
     //    [t*WPT, (t+1)*WPT) (vector loads), one block-wide scan of the thread
     //    totals.  Each word becomes (start(2w), start(2w+1)).

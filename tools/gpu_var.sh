@@ -1,5 +1,7 @@
-# timing of several compile variants: gpu_var.sh "<flags1>" "<flags2>" ...  (ARGS = prof_run args)
-for v in "$@"; do
-IPS4O_EXTRA_NVCC_FLAGS="$v" python -m paper_2009_13569_b200.build --force > gpurun_out/build.log 2>&1 || { tail -3 gpurun_out/build.log; exit 1; }
-echo "== [$v]"; python tools/prof_run.py ${ARGS:---n 30 --reps 2} 2>&1 | grep -v "^0 " | cut -c1-220
+# timing of several build variants: gpu_var.sh "<prof_run args>" "<flags A>" "<flags B>" ...
+ARGS=$1; shift
+for V in "$@"; do
+  IPS4O_EXTRA_NVCC_FLAGS="$V" python -m paper_2009_13569_b200.build --force > gpurun_out/build_v.log 2>&1 || { echo "build failed: $V"; tail -5 gpurun_out/build_v.log; continue; }
+  echo "variant: [$V]"
+  timeout 300 python tools/prof_run.py $ARGS 2>&1 | tail -1
 done
