@@ -90,6 +90,8 @@ struct LevelArgs {
   char *overflow;             // [ntasks][b*D] overflow blocks
   u32 *ovf_used;              // [ntasks] bucket that wrote the overflow block, or ~0
   unsigned char *rdone;       // [blk_off + x] block x of the task has been read (K4)
+  unsigned short *bid;        // [blk_off + x] bucket of the full block at x (K2 writes,
+                              // K3 moves with the block, K4 reads)
   u32 *task_done;             // [ntasks] no block of the task can be fetched any more (K4)
   // scheduler outputs
   TaskDesc *next_tasks;       // next level

@@ -182,6 +182,7 @@ static void layout(LevelArgs &A, Arena &ar, const LevelPlan &P) {
   A.overflow = ar.take<char>(T * (size_t)B * D);
   A.ovf_used = ar.take<u32>(T);
   A.rdone = ar.take<unsigned char>(P.nblk);
+  A.bid = ar.take<unsigned short>(P.nblk);
   A.task_done = ar.take<u32>(T);
   A.minmax = ar.take<u64>(2);
   A.measure_part = ar.take<u32>(P.measure_part.size());
@@ -957,6 +958,7 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
   add(T * BD);
   add(T * 4);
   add(n / B + 2 * T);                   // read-done flags
+  add(2 * (n / B + 2 * T));             // block buckets
   add(T * 4);                           // task_done
   add(16);                              // minmax
   const u64 MP = T + n / MEAS_PART_ELEMS + 1;  // K0m parts

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
       const u32 bf = s_fill[j];
       const u32 eo = s_eoff[j];
       Unit *dst = reinterpret_cast<Unit *>(gtask + (s0 + (front + s_boff[j] + q) * B) * D);
+      if (lane == 0) A.bid[L.blk_off + s0 / B + front + s_boff[j] + q] = (unsigned short)j;
       for (int u = lane; u < B * UPE; u += 32) {
         const int e = u / UPE, w = u - e * UPE;
         const u32 v = q * B + e;
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelAr
       const u32 bf = (u32)(pl & 0xFFFFu);
       const u32 eo = (u32)(pl >> 32);
       Unit *dst = gtask + s0 + (front + g) * B;
+      if (lane == 0) A.bid[L.blk_off + s0 / B + front + g] = (unsigned short)j;
 #pragma unroll
       for (int e = lane; e < B; e += 32) {
         const u32 v = q * B + e;
@@ -722,6 +724,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   Key kmin = key_max<Key>(), kmax = (Key)0;
 
   const u64 n = s1 > s0 ? s1 - s0 : 0;
+  unsigned short *const bidp = A.bid + L.blk_off + s0 / B;  // block buckets of this stripe (K4)
   const u64 ntiles = (n + T - 1) / T;
   u64 front = 0;
   Unit x[IPT], y[IPT], xl[IPT];
@@ -886,6 +889,12 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
         Unit *dst = gtask + s0 + (front + g) * B;
 #pragma unroll
         for (int e = 0; e < B / 16; ++e) dst[hl + 16 * e] = src[hl + 16 * e];
+      }
+      // the buckets of the emitted blocks, for K4 (coalesced 2-byte stores by
+      // the last warp; warp 0 issues the prefetches)
+      if (wid == NWARPS - 1) {
+#pragma unroll 1
+        for (u32 g = lane; g < nblocks; g += 32) bidp[front + g] = (unsigned short)(s_blkb[g] & 0x1FFu);
       }
     }
     front += nblocks;

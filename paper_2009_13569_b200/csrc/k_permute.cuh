@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
       const Unit *s = reinterpret_cast<const Unit *>(gtask + src * B * D);
       Unit *d = reinterpret_cast<Unit *>(gtask + dstb * B * D);
       for (int u = lane; u < NU; u += 32) d[u] = s[u];
+      if (lane == 0) A.bid[L.blk_off + dstb] = A.bid[L.blk_off + src];
     }
   }
 }
@@ -196,8 +197,20 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
 // completed, and a writer that targets a formerly full position waits on that
 // byte with acquire loads.  Same guarantee, no shared counters, no fences
 // (DESIGN "Permutation on the GPU").
+//
+// The bucket of a block is not recomputed from its first key: K2 records it
+// per block position when it flushes the block (K3 moves it with the block),
+// so an agent learns where a swapped-out block goes from a 2-byte load that
+// returns long before the block, and issues the next atomic while the block
+// is still in flight.
 constexpr int PERM_WARPS = 8;
+#ifndef IPS4O_PERM_MINB
+#define IPS4O_PERM_MINB 8  // full occupancy: 32 registers (a few bytes spill)
+#endif
 constexpr u32 PERM_HOP_WINDOW = 64;  // tasks an idle agent may look ahead
+#ifndef IPS4O_PERM_TREE_PACE_NS
+#define IPS4O_PERM_TREE_PACE_NS 0
+#endif
 #ifndef IPS4O_PERM_DIGIT_PACE_NS
 #define IPS4O_PERM_DIGIT_PACE_NS 100
 #endif
@@ -284,25 +297,15 @@ __device__ __forceinline__ u32 ld_relaxed_u32(const u32 *p) {
 // own agents are done.  The protocol per task is unchanged; it does not care
 // which agents take part.
 template <int DT, int ALGO>
-__global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
+__global__ void __launch_bounds__(PERM_THREADS, IPS4O_PERM_MINB) permute_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
   using Key = typename Tr::Key;
   using Unit = typename Tr::Unit;
   constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX;
   constexpr int NU = B * D / (int)sizeof(Unit);
   constexpr int NPL = (NU + 31) / 32;
-  __shared__ Key s_tree[KI], s_spl[KI];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u32 home = A.perm_task[blockIdx.x];
-  if (ALGO == ALGO_TREE) {
-    const LevelTask &H = A.tasks[home];
-    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)home * 2 * KI;
-    for (int i = threadIdx.x; i < (1 << H.l); i += PERM_THREADS) {
-      s_tree[i] = gt[i];
-      s_spl[i] = gt[KI + i];
-    }
-  }
-  __syncthreads();
   if (A.dbg_one_agent && wid != 0) return;
   const u32 agent = (blockIdx.x - A.tasks[home].perm_first) * PERM_WARPS + wid;
   PCLK_DECL
@@ -328,21 +331,20 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
       ti = nxt;
     }
     const LevelTask &L = A.tasks[ti];
-    const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
+    const int K = (int)L.K, shift = L.shift;
+    const u32 dmask = L.K - 1;
     if (K <= 1) {
       if (lane == 0) atomicExch(&A.task_done[ti], 1u);
       continue;
     }
-    const u32 dmask = L.K - 1;
     const bool local = ti == home;
-    const Key *tr = local ? s_tree : reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
-    const Key *sp = local ? s_spl : tr + KI;
     char *gtask = A.base + L.t.begin * (u64)D;
     const u64 size = L.t.size;
     const u64 pblk = (size % B) ? size / B : ~0ull;  // partial last block -> overflow
     char *ovf = A.overflow + (size_t)ti * B * D;
     u64 *wr = A.wr + L.bucket_off * WR_STRIDE;
     unsigned char *rdone = A.rdone + L.blk_off;
+    const unsigned short *bid = A.bid + L.blk_off;  // bucket of each full block (K2/K3)
     const u32 nagents = A.dbg_one_agent ? 1 : L.nperm * PERM_WARPS;
     // P:847 starting points spread over the buckets
     int p = local ? (int)(((u64)agent * (u64)K) / nagents) : (int)((agent * 97u + blockIdx.x) % (u32)K);
@@ -368,28 +370,79 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
         if (u < NU) d[u] = r[i];
       }
     };
-    // bucket of the block held in registers: its key is in the first
-    // KEY_UNITS units, i.e. on lanes 0..KEY_UNITS-1 of register 0
-    auto bucket_of = [&](const Unit(&r)[NPL]) -> u32 {
-      Unit ku[Tr::KEY_UNITS];
-      if constexpr (Tr::KEY_UNITS == 1) {
-        ku[0] = r[0];
-      } else {
+    // Pacing: with nothing between a block's arrival and the next atomic,
+    // agents of the digit path return to the hot (w, r) words so fast that
+    // same-address atomics queue up at L2 and every step slows ~10x
+    // (measured: 7100-cycle atomics vs ~650 with a ~100 ns gap).
+    // The digit path therefore takes a block's bucket from its first key
+    // once the block has arrived (one shift), and sleeps briefly.
+    auto bucket = [&](u32 bv, const Unit(&r)[NPL]) -> u32 {
+      if constexpr (ALGO == ALGO_DIGIT) {
+        Unit ku[Tr::KEY_UNITS];
+        if constexpr (Tr::KEY_UNITS == 1) {
+          ku[0] = r[0];
+        } else {
 #pragma unroll
-        for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = shfl_unit(r[0], q);
+          for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = shfl_unit(r[0], q);
+        }
+        if (lane == 0) {
+          bv = digit_of(Tr::key(reinterpret_cast<const char *>(ku)), shift, dmask);
+          __nanosleep(PERM_DIGIT_PACE_NS);
+        }
+      } else {
+#if IPS4O_PERM_TREE_PACE_NS > 0
+        if (lane == 0) __nanosleep(IPS4O_PERM_TREE_PACE_NS);  // tuning experiment
+#endif
       }
-      u32 b = 0;
+      return __shfl_sync(0xffffffffu, bv, 0);
+    };
+    // Place the block held in `hold` (bucket dest): w += 1 on dest; an
+    // unprocessed block at w is swapped out into `spare` (its bucket comes
+    // from the block-bucket array, so the next atomic is issued while the
+    // block itself is still in flight) unless it already belongs to dest
+    // (P:902-903); an empty block at w is written once its reader is done
+    // (P:898).  Returns 0 = placed, 1 = swapped (spare now holds
+    // the block to place, dest its bucket), 2 = skipped (hold unchanged).
+    auto place = [&](Unit(&hold)[NPL], Unit(&spare)[NPL], u32 &dest) -> int {
+      u64 old = 0;
+      PCLK_START();
+      if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
+      old = __shfl_sync(0xffffffffu, old, 0);
+      PCLK_ADD(1);
+      PCLK_CNT(4);
+      const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
+      if (w <= r) {
+        PCLK_START();
+        const u32 bv = ALGO == ALGO_TREE && lane == 0 ? (u32)__ldg(bid + w) : 0u;
+        load_blk((u64)w, spare);
+        const u32 b2 = bucket(bv, spare);
+        PCLK_ADD(2);
+        if (b2 == dest) {
+          if (lane == 0) PSTAT(4, 1);
+          return 2;
+        }
+        if (lane == 0) PSTAT(3, 1);
+        store_blk((u64)w, hold);  // the loads of block w precede this store (same lanes, same addresses)
+        dest = b2;
+        return 1;
+      }
+      PCLK_START();
       if (lane == 0) {
-        Key k = Tr::key(reinterpret_cast<const char *>(ku));
-        b = ALGO == ALGO_TREE ? tree_bucket<Key>(tr, sp, l, eq, k) : digit_of(k, shift, dmask);
-        // Pacing: with the one-instruction digit, agents return to the hot
-        // (w, r) words so fast that same-address atomics queue up at L2 and
-        // every step slows ~10x (measured: 7100-cycle atomics, 7600-cycle
-        // loads per step vs ~650/2400 with a ~100 ns gap; the tree walk
-        // provides that gap by itself).
-        if (ALGO == ALGO_DIGIT) __nanosleep(PERM_DIGIT_PACE_NS);
+        const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
+        PSTAT(5, 1);
+        if ((u64)w < pe) {
+          PSTAT(6, 1);
+          while (ld_acquire_u8(rdone + w) == 0) {
+            PSTAT(7, 1);
+            __nanosleep(32);
+          }
+        }
+        if ((u64)w == pblk) A.ovf_used[ti] = dest;
       }
-      return __shfl_sync(0xffffffffu, b, 0);
+      __syncwarp();
+      PCLK_ADD(3);
+      store_blk((u64)w, hold);
+      return 0;
     };
 
     Unit buf0[NPL], buf1[NPL];
@@ -437,7 +490,9 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
       }
       if (x == ~0ull) break;
       PCLK_ADD(0);
+      const u32 bx = ALGO == ALGO_TREE && lane == 0 ? (u32)__ldg(bid + x) : 0u;
       load_blk(x, buf0);
+      u32 dest = bucket(bx, buf0);
       {
         // every lane's loads have returned once the reduction has its
         // operands; then publish "block x read" (release) for a writer
@@ -448,52 +503,13 @@ __global__ void __launch_bounds__(PERM_THREADS) permute_kernel(LevelArgs A) {
         asm volatile("" ::"r"(v));  // keep the dependency on every lane's loads
         if (lane == 0) st_release_u8(rdone + x, 1u);
       }
-      u32 dest = bucket_of(buf0);
-      // ---- place buf0 into dest, swapping while dest has unprocessed blocks
+      // ---- place it, swapping while dest has unprocessed blocks; the two
+      //      register buffers alternate roles (no copies between them)
+      bool in1 = false;
       for (;;) {
-        u64 old = 0;
-        PCLK_START();
-        if (lane == 0) old = atomicAdd(&wr[(u64)dest * WR_STRIDE], 1ull << 32);  // w += 1
-        old = __shfl_sync(0xffffffffu, old, 0);
-        PCLK_ADD(1);
-        PCLK_CNT(4);
-        const i64 w = (i64)(old >> 32), r = (i64)(old & 0xFFFFFFFFull) - (i64)RBIAS;
-        if (w <= r) {
-          // unprocessed block at w: swap, or skip it if already in place
-          PCLK_START();
-          load_blk((u64)w, buf1);
-          const u32 b2 = bucket_of(buf1);
-          PCLK_ADD(2);
-          if (b2 == dest) {
-            if (lane == 0) PSTAT(4, 1);
-            continue;
-          }
-          if (lane == 0) PSTAT(3, 1);
-          store_blk((u64)w, buf0);
-#pragma unroll
-          for (int i = 0; i < NPL; ++i) buf0[i] = buf1[i];
-          dest = b2;
-          continue;
-        }
-        // empty block at w.  If it was full before the permutation,
-        // its reader must be done.
-        PCLK_START();
-        if (lane == 0) {
-          const u64 pe = wr[(u64)dest * WR_STRIDE + 1];  // prefix end of region dest
-          PSTAT(5, 1);
-          if ((u64)w < pe) {
-            PSTAT(6, 1);
-            while (ld_acquire_u8(rdone + w) == 0) {
-              PSTAT(7, 1);
-              __nanosleep(32);
-            }
-          }
-          if ((u64)w == pblk) A.ovf_used[ti] = dest;
-        }
-        __syncwarp();
-        PCLK_ADD(3);
-        store_blk((u64)w, buf0);
-        break;
+        const int st = in1 ? place(buf1, buf0, dest) : place(buf0, buf1, dest);
+        if (st == 0) break;
+        if (st == 1) in1 = !in1;
       }
     }
     if (lane == 0) atomicExch(&A.task_done[ti], 1u);
