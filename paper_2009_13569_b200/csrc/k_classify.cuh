@@ -614,9 +614,9 @@ template <int DT> struct ClsV2 {
   // u32 arrays: tcnt, cnt, plan (KI each), ws (32); then the block -> (bucket, index) map
   static constexpr size_t off_blkb = off_u32 + (3 * KI + 32) * 4;
   static constexpr int MAXBLK = T / B + KI;
-  static constexpr int LUT_BITS = 13;
+  static constexpr int LUT_BITS = 14;  // 16-bit entries
   static constexpr size_t off_lut = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
-  static constexpr size_t bytes = off_lut + ((size_t)4 << LUT_BITS);
+  static constexpr size_t bytes = off_lut + ((size_t)2 << LUT_BITS);
 };
 
 template <int DT, int ALGO>
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   u32 *s_plan = s_cnt + KI;
   u32 *s_ws = s_plan + KI;
   unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
-  u32 *s_lut = reinterpret_cast<u32 *>(smem + S::off_lut);
+  unsigned short *s_lut = reinterpret_cast<unsigned short *>(smem + S::off_lut);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u32 stripe = blockIdx.x;
@@ -668,9 +668,11 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   }
   u32 myfill = 0;  // tid < KI: elements buffered for bucket tid
 
-  // Lookup table of starting leaves (see classify_reg_kernel): slot q covers
-  // [llo + q*2^ls, llo + (q+1)*2^ls) and stores a = #{splitters < its first
-  // key} and the number of splitters inside it (inclusive of its last key).
+  // Lookup table of starting leaves: slot q covers
+  // [llo + q*2^ls, llo + (q+1)*2^ls).  A 16-bit entry holds either the final
+  // bucket (FIN, no splitter in the slot) or a = #{splitters < its first key}
+  // (9 bits) and the number c of splitters inside it (6 bits, 63 = "63 or
+  // more"): c = 1, the common case, takes one comparison.
   const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
   Key llo = tlo, lhi = thi;
   if (ALGO == ALGO_TREE) {
@@ -693,7 +695,8 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   if (ls < 0) ls = 0;
   const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
   const int nspl = (1 << l) - 1;
-  constexpr u32 FIN = 1u << 31;  // table entry holds the final bucket
+  constexpr u32 FIN = 1u << 15;  // table entry holds the final bucket
+  static_assert(KI <= 512, "bucket and splitter indices fit 9 bits");
   if (ALGO == ALGO_TREE) {
     __syncthreads();
     auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
@@ -715,9 +718,9 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
         const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
         // no splitter in the slot: no key in it equals one, so key < s_a,
         // except above the last splitter (bucket 2s+1 with equality buckets)
-        e = b == a ? FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | ((b - a) << 16);
+        e = b == a ? FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | (min(b - a, 63u) << 9);
       }
-      s_lut[q] = e;
+      s_lut[q] = (unsigned short)e;
     }
   }
   const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
@@ -798,15 +801,27 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
           if (ent[k] & FIN) {
-            bkt[k] = ent[k] & 0xFFFFu;
+            bkt[k] = ent[k] & 0x3FFu;
           } else {  // the slot holds splitters: lower bound among them
-            u32 a = ent[k] & 0xFFFFu, b = a + (ent[k] >> 16);
-            while (a < b) {
-              const u32 mid = (a + b) >> 1;
-              if (s_spl[mid] < key[k]) a = mid + 1;
-              else b = mid;
+            const u32 a0 = ent[k] & 0x1FFu, c = ent[k] >> 9;
+            const Key sv = s_spl[a0];
+            if (c == 1) {
+              // one splitter s_a0 in the slot; the next one lies above it
+              if (sv < key[k]) {
+                const u32 a1 = a0 + 1;
+                bkt[k] = eq ? 2 * a1 + (a1 == (u32)nspl ? 1u : 0u) : a1;
+              } else {
+                bkt[k] = eq ? 2 * a0 + 1 - (key[k] < sv ? 1u : 0u) : a0;
+              }
+            } else {
+              u32 a = a0, b = c == 63 ? (u32)nspl : a0 + c;
+              while (a < b) {
+                const u32 mid = (a + b) >> 1;
+                if (s_spl[mid] < key[k]) a = mid + 1;
+                else b = mid;
+              }
+              bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
             }
-            bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
           }
         }
       } else {
