@@ -285,11 +285,35 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   constexpr int TDW = sizeof(TaskDesc) / 4;
   static_assert(TDW <= 32 && sizeof(TaskDesc) % 4 == 0, "one word per lane");
   __shared__ TaskDesc s_task[2];
+  // The digit parameters of a bucket (see below) are computed once, by thread
+  // 0, for the NEXT bucket while the current one is sorted.
+  struct DigitPar {
+    int ds, nd, direct, exact;
+    u32 dmul, pad;
+  };
+  __shared__ DigitPar s_par[2];
+  auto digit_par = [&](const TaskDesc &tt, DigitPar &P) {
+    const int mm = (int)tt.size;
+    int lg = 1;
+    while ((1 << lg) < mm && lg < BI::DBMAX) ++lg;
+    const Key range = key_from_words<Key>(tt.hi) - key_from_words<Key>(tt.lo);
+    const int bits = bitlen(range);
+    const int ds = bits > 32 ? bits - 32 : 0;
+    const u32 r32 = (u32)(range >> ds);
+    const bool direct = r32 < (1u << lg);
+    P.ds = ds;
+    P.nd = direct ? (int)r32 + 1 : (1 << lg);
+    P.direct = direct;
+    P.exact = direct && ds == 0;  // a digit holds a single key value
+    P.dmul = direct ? 1u : (u32)((1ull << (32 + lg)) / ((u64)r32 + 1));
+  };
   u32 tdw = 0;
   if (blockIdx.x < count) {
     if (tid < TDW) reinterpret_cast<u32 *>(&s_task[0])[tid] = reinterpret_cast<const u32 *>(&tasks[blockIdx.x])[tid];
     __syncthreads();
+    if (tid == 0) digit_par(s_task[0], s_par[0]);
     prefetch_l2(base + s_task[0].begin * (u64)D, s_task[0].size * (u64)D, tid, NT);
+    __syncthreads();
   }
   int cur = 0;
   for (u32 ti = blockIdx.x; ti < count; ti += gridDim.x, cur ^= 1) {
@@ -305,6 +329,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     if (m <= 1 || !(lo < hi)) {
       publish_next();
       __syncthreads();
+      if (has_next && tid == 0) digit_par(s_task[cur ^ 1], s_par[cur ^ 1]);
+      __syncthreads();
       continue;
     }
     // digit(x) = floor(v(x) * dmul / 2^32) with v(x) = the top 32 bits of
@@ -312,21 +338,16 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     // needs; the runs are finished by key comparisons) and spread evenly over
     // nd digits, ~1 element per digit (nd = pow2 >= m).  Ranges narrower than
     // nd use v itself (one key per digit when ds == 0).
-    int lg = 1;
-    while ((1 << lg) < m && lg < BI::DBMAX) ++lg;
-    const Key range = hi - lo;
-    const int bits = bitlen(range);
-    const int ds = bits > 32 ? bits - 32 : 0;
-    const u32 r32 = (u32)(range >> ds);
-    const bool direct = r32 < (1u << lg);
-    const int nd = direct ? (int)r32 + 1 : (1 << lg);
-    const bool exact = direct && ds == 0;  // a digit holds a single key value
-    const u32 dmul = direct ? 1u : (u32)((1ull << (32 + lg)) / ((u64)r32 + 1));
+    const DigitPar &par = s_par[cur];
+    const int ds = par.ds, nd = par.nd;
+    const bool direct = par.direct != 0, exact = par.exact != 0;
+    const u32 dmul = par.dmul;
     auto digit = [&](const Item &it) -> u32 {
       const u32 v = (u32)((BI::key(it) - lo) >> ds);
       return direct ? v : __umulhi(v, dmul);
     };
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
+    BC_PHASE(7)
     for (int w = tid; w < (1 << BI::DBMAX) / 8; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
       s_nbig = 0;
@@ -365,6 +386,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     publish_next();
     __syncthreads();
     BC_PHASE(1)
+    if (has_next && tid == 0) digit_par(s_task[cur ^ 1], s_par[cur ^ 1]);  // visible after the scan
     // the next bucket of this CTA streams into L2 while this one is sorted
     if (has_next) prefetch_l2(base + s_task[cur ^ 1].begin * (u64)D, s_task[cur ^ 1].size * (u64)D, tid, NT);
     // 2. exclusive scan in place: thread t owns the WPT consecutive words
@@ -497,8 +519,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         u64 lw[3], hw[3];
         key_to_words<Key>(lo, lw);
         key_to_words<Key>(hi, hw);
-        printf("bc task %u m %d pass %d lo %llx:%llx:%llx hi %llx:%llx:%llx bits %d ds %d nd %d nbig %u bigsum %u whole %d\n",
-               ti, m, pass, lw[2], lw[1], lw[0], hw[2], hw[1], hw[0], bits, ds, nd, s_nbig, s_bigsum, (int)whole);
+        printf("bc task %u m %d pass %d lo %llx:%llx:%llx hi %llx:%llx:%llx ds %d nd %d nbig %u bigsum %u whole %d\n",
+               ti, m, pass, lw[2], lw[1], lw[0], hw[2], hw[1], hw[0], ds, nd, s_nbig, s_bigsum, (int)whole);
       }
 #endif
       if (whole) {
@@ -555,14 +577,15 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
           if (lane < D / 4) out[(size_t)i * (D / 4) + lane] = src[lane];
         }
       }
-      __syncthreads();
       BC_PHASE(5)
+      __syncthreads();
+      BC_PHASE(6)
     }
   }
 #ifdef IPS4O_PHASE_TIMING
   if (tid == 0 && blockIdx.x == 0)
-    printf("basecase CTA0 cycles: zero %lld hist %lld scan %lld scatter %lld big %lld rank+write %lld\n", ph_[0],
-           ph_[1], ph_[2], ph_[3], ph_[4], ph_[5]);
+    printf("basecase CTA0 cycles: setup %lld zero %lld hist %lld scan %lld scatter %lld big %lld rank+write %lld endbar %lld\n",
+           ph_[7], ph_[0], ph_[1], ph_[2], ph_[3], ph_[4], ph_[5], ph_[6]);
 #endif
 }
 
