@@ -34,8 +34,19 @@ def sources():
         os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "ips4o.h")]
 
 
+STAMP = os.path.join(HERE, "lib", "extra_flags.txt")
+
+
+def extra_flags():
+    return os.environ.get("IPS4O_EXTRA_NVCC_FLAGS", "").split()  # e.g. -DIPS4O_PHASE_TIMING
+
+
 def stale() -> bool:
     if not os.path.exists(OUT):
+        return True
+    # a library built with other extra flags (a tuning or debug variant) is stale
+    built_with = open(STAMP).read().split() if os.path.exists(STAMP) else []
+    if built_with != extra_flags():
         return True
     t = os.path.getmtime(OUT)
     return any(os.path.getmtime(s) > t for s in sources())
@@ -45,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    extra = os.environ.get("IPS4O_EXTRA_NVCC_FLAGS", "").split()  # e.g. -DIPS4O_PHASE_TIMING
+    extra = extra_flags()
     cmd = [NVCC, *FLAGS, *extra, "-o", OUT, SRC, "-lrt", "-ldl", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "lib", "build.log")
@@ -54,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-8000:])
         raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+    with open(STAMP, "w") as f:
+        f.write(" ".join(extra) + "\n")
     if verbose:
         sys.stderr.write(res.stderr)
     return OUT
