@@ -6,8 +6,9 @@
 //      into ~m nearly equal runs of ~1 element; 16-bit counters),
 //   2. exclusive scan and scatter into shared memory (the second read of the
 //      bucket hits L2),
-//   3. runs longer than RANKMAX are sorted in place by a warp bitonic network,
-//   4. every element computes its rank inside its (short) run by counting the
+//   3. runs longer than RW + 1 are sorted in place by a warp (warp_sort_run),
+//   4. every element computes its rank inside its short run (<= RW + 1, a fixed
+//      window of neighbours) by counting the
 //      smaller elements -- the parallel form of the paper's insertion-sort
 //      base case -- and is written straight to its final global position.
 #pragma once
@@ -87,8 +88,9 @@ template <> struct BaseItem<DT_REC100> {
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
 };
 
-constexpr int RANKMAX = 32;  // longer runs are sorted by a warp bitonic network
-constexpr int BIGCAP = 256;  // long runs listed per bucket (more: digit scan fallback)
+constexpr int RW = 3;        // rank window: runs of up to RW + 1 elements are ranked in registers
+constexpr int RANKMAX = 32;  // runs this long count towards the whole-bucket fallback
+constexpr int BIGCAP = 512;  // runs longer than RW + 1 listed per bucket (more: digit scan fallback)
 
 template <int DT> struct BaseSmem {
   using BI = BaseItem<DT>;
@@ -133,14 +135,30 @@ __device__ void warp_bitonic_run(typename BI::Item *a, int n, int lane) {
   }
 }
 
-// A run longer than RANKMAX (SIMD warp per run): nothing to do if all its
-// keys are equal (any order of equal keys is a sorted result); for key-only
-// items a run of at most 8 distinct keys is rewritten by counting them
+// A run longer than the rank window (SIMD warp per run): nothing to do if all
+// its keys are equal (any order of equal keys is a sorted result); up to 32
+// elements are ranked by counting, one per lane; longer runs of key-only
+// items with at most 8 distinct keys are rewritten by counting the keys
 // (duplicate-heavy inputs: TwoDup, EightDup); otherwise a bitonic sort.
 template <class BI>
 __device__ void warp_sort_run(typename BI::Item *a, int n, int lane) {
   using Item = typename BI::Item;
   using Key = typename BI::Key;
+  if (n <= 32) {
+    // one element per lane, ranked by counting (ties by position); nothing
+    // to do if all keys are equal
+    const Item x = a[lane < n ? lane : 0];
+    if (__all_sync(0xffffffffu, BI::key(x) == BI::key(a[0]))) return;
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const Item y = a[j];
+      r += (BI::less(y, x) || (!BI::less(x, y) && j < lane)) ? 1 : 0;
+    }
+    __syncwarp();
+    if (lane < n) a[r] = x;
+    __syncwarp();
+    return;
+  }
   const Key k0 = BI::key(a[0]);
   bool diff = false;
   for (int i = lane; i < n; i += 32) diff |= BI::key(a[i]) != k0;
@@ -417,17 +435,17 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       for (int q = 0; q < WPT; ++q) {
         const u32 c0 = h[q] & 0xFFFFu, c1 = h[q] >> 16;
         const u32 w = (u32)(tid * WPT + q);
-        // runs longer than RANKMAX are listed for the warp bitonic sort
-        if (!exact && (c0 > RANKMAX || c1 > RANKMAX) && w < (u32)nw) {
-          if (c0 > RANKMAX) {
+        // runs longer than RW + 1 are listed for the warp sort
+        if (!exact && (c0 > RW + 1 || c1 > RW + 1) && w < (u32)nw) {
+          if (c0 > RW + 1) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w;
-            atomicAdd(&s_bigsum, c0);
+            if (c0 > RANKMAX) atomicAdd(&s_bigsum, c0);
           }
-          if (c1 > RANKMAX) {
+          if (c1 > RW + 1) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
-            atomicAdd(&s_bigsum, c1);
+            if (c1 > RANKMAX) atomicAdd(&s_bigsum, c1);
           }
         }
         h[q] = st | ((st + c0) << 16);
@@ -538,7 +556,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
           for (int d = dlo + wid; d < dhi; d += NT / 32) {
             const int a = d ? (int)s_end[d - 1] : 0;
             const int n = (int)s_end[d] - a;
-            if (n > RANKMAX) warp_sort_run<BI>(s_items + (a - off), n, lane);
+            if (n > RW + 1) warp_sort_run<BI>(s_items + (a - off), n, lane);
           }
         }
         if (nbig) __syncthreads();
@@ -552,11 +570,17 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         const int a = (d ? (int)s_end[d - 1] : 0) - off;
         const int b = (int)s_end[d] - off;
         int rank = i - a;
-        if (!exact && !whole && b - a > 1 && b - a <= RANKMAX) {
+        if (!exact && !whole && b - a > 1 && b - a <= RW + 1) {
+          // the run lies inside [i - RW, i + RW]: a fixed, branch-free window
+          // (ties by position)
           rank = 0;
-          for (int j = a; j < b; ++j) {
-            const Item y = s_items[j];
-            rank += (BI::less(y, it) || (!BI::less(it, y) && j < i)) ? 1 : 0;
+#pragma unroll
+          for (int o = -RW; o <= RW; ++o) {
+            const int j = i + o;
+            if (o != 0 && j >= a && j < b) {
+              const Item y = s_items[j];
+              rank += (o < 0 ? !BI::less(it, y) : BI::less(y, it)) ? 1 : 0;
+            }
           }
         }
         const int pos = off + a + rank;
