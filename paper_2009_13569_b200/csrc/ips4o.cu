@@ -391,7 +391,8 @@ static int run_level(Ctx &c, char *base, std::vector<TaskDesc> &tasks, std::vect
   A.algo = ALGO;
   A.seed = c.seed;
   A.base_cap_elems = c.base_cap;
-  A.base_split_elems = BaseItem<DT>::SPLIT ? 2 * c.base_cap : c.base_cap;
+  // (16-bit run counters: a split bucket stays below 2^16 elements)
+  A.base_split_elems = BaseItem<DT>::SPLIT ? std::min<u64>(2 * c.base_cap, 65535) : c.base_cap;
   A.dbg_one_agent = c.dbg_one_agent ? 1 : 0;
   // upload the plan (tasks, stripe->task, perm->task) through pinned staging
   const size_t T = P.lt.size(), S = P.stripe_task.size(), NP = P.perm_task.size();

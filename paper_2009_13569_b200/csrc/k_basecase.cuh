@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
   char *s_rec = smem + S::off_rec;
   unsigned short *s_sidx = reinterpret_cast<unsigned short *>(smem + S::off_sidx);
-  u32 *s_hist = reinterpret_cast<u32 *>(smem + S::off_hist);
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
   __shared__ u32 s_nbig, s_bigsum, s_dsplit, s_scnt;
@@ -307,8 +306,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   // 0, for the NEXT bucket while the current one is sorted.
   struct DigitPar {
     int ds, nd, direct, exact;
-    u32 dmul, pad;
+    u32 dmul, hoff;  // hoff: byte offset of the counters in shared memory
+    int nwz, pad;    // nwz: counter words to clear (multiple of 4)
   };
+  constexpr int HSTAT = (1 << BI::DBMAX) / 2;  // counter words of the static area
   __shared__ DigitPar s_par[2];
   auto digit_par = [&](const TaskDesc &tt, DigitPar &P) {
     const int mm = (int)tt.size;
@@ -318,7 +319,26 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     const int bits = bitlen(range);
     const int ds = bits > 32 ? bits - 32 : 0;
     const u32 r32 = (u32)(range >> ds);
-    const bool direct = r32 < (1u << lg);
+    bool direct = r32 < (1u << lg);
+    P.hoff = (u32)S::off_hist;
+    P.nwz = HSTAT;
+    if constexpr (!BI::STAGE_RECORDS) {
+      // A narrow key range (duplicate-heavy inputs) is counted exactly, one
+      // counter per key value, when the counters fit the static area plus the
+      // unused tail of the item array (the counters then start below it).
+      if (!direct && ds == 0 && r32 < (1u << BI::DBMAX)) {
+        direct = true;  // the static area holds the r32 + 1 counters
+      } else if (!direct && ds == 0) {
+        const u64 used = (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
+        const u64 hb = (((u64)r32 / 2 + 1) * 4 + 15) & ~15ull;  // bytes for r32 + 1 counters
+        const u64 hend = S::off_hist + (u64)HSTAT * 4;
+        if (hend >= hb && hend - hb >= S::off_items + used) {
+          direct = true;
+          P.hoff = (u32)(hend - hb);
+          P.nwz = (int)(hb / 4);
+        }
+      }
+    }
     P.ds = ds;
     P.nd = direct ? (int)r32 + 1 : (1 << lg);
     P.direct = direct;
@@ -365,8 +385,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       return direct ? v : __umulhi(v, dmul);
     };
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
+    u32 *s_hist = reinterpret_cast<u32 *>(smem + par.hoff);
+    const bool hbig = nw > HSTAT;  // exact counters beyond the static area
     BC_PHASE(7)
-    for (int w = tid; w < (1 << BI::DBMAX) / 8; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
+    for (int w = tid; w < par.nwz / 4; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
       s_nbig = 0;
       s_bigsum = 0;
@@ -410,7 +432,20 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     // 2. exclusive scan in place: thread t owns the WPT consecutive words
     //    [t*WPT, (t+1)*WPT) (vector loads), one block-wide scan of the thread
     //    totals.  Each word becomes (start(2w), start(2w+1)).
-    {
+    if (hbig) {
+      // exact counters (no long runs): contiguous words per thread, two passes
+      const int wpt = (nw + NT - 1) / NT;
+      const int w0 = min(tid * wpt, nw), w1 = min(w0 + wpt, nw);
+      u32 tot = 0;
+      for (int w = w0; w < w1; ++w) tot += (s_hist[w] & 0xFFFFu) + (s_hist[w] >> 16);
+      u32 all;
+      u32 st = block_exclusive_scan<NT>(tot, s_ws, &all);
+      for (int w = w0; w < w1; ++w) {
+        const u32 h = s_hist[w], c0 = h & 0xFFFFu, c1 = h >> 16;
+        s_hist[w] = st | ((st + c0) << 16);
+        st += c0 + c1;
+      }
+    } else {
       constexpr int WPT = ((1 << BI::DBMAX) / 2 + NT - 1) / NT;
       u32 h[WPT];
       if constexpr (WPT % 4 == 0) {
