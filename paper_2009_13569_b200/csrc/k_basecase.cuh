@@ -88,6 +88,16 @@ template <> struct BaseItem<DT_REC100> {
   __device__ static bool less(const Item &a, const Item &b) { return a < b; }
 };
 
+// Widest key range (hi - lo) a key-only bucket can be counted exactly with
+// (one 16-bit counter per key value over the whole shared-memory area; see
+// digit_par in basecase_kernel); K6 sends such buckets of up to 65535
+// elements to the base case whatever their size.
+template <int DT> struct BaseSmem;
+template <int DT> constexpr unsigned long long basecase_count_range() {
+  return BaseItem<DT>::KEY_ONLY ? (unsigned long long)(BaseSmem<DT>::off_hist + ((size_t)1 << BaseItem<DT>::DBMAX) * 2) / 2 - 16
+                                : 0ull;
+}
+
 constexpr int RW = 3;        // rank window: runs of up to RW + 1 elements are ranked in registers
 constexpr int RANKMAX = 32;  // runs this long count towards the whole-bucket fallback
 constexpr int BIGCAP = 512;  // runs longer than RW + 1 listed per bucket (more: digit scan fallback)
@@ -329,7 +339,9 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       if (!direct && ds == 0 && r32 < (1u << BI::DBMAX)) {
         direct = true;  // the static area holds the r32 + 1 counters
       } else if (!direct && ds == 0) {
-        const u64 used = (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
+        // (key-only items are then written from the counts alone: no item
+        // array at all)
+        const u64 used = BI::KEY_ONLY ? 0 : (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
         const u64 hb = (((u64)r32 / 2 + 1) * 4 + 15) & ~15ull;  // bytes for r32 + 1 counters
         const u64 hend = S::off_hist + (u64)HSTAT * 4;
         if (hend >= hb && hend - hb >= S::off_items + used) {
@@ -499,6 +511,42 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     __syncthreads();
     BC_PHASE(2)
     const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // starts, ends after the scatter
+    if constexpr (BI::KEY_ONLY) {
+      if (exact) {
+        // One key value per digit and nothing but the key in an item: the
+        // counts alone are the sorted bucket.  Digit d fills [start_d,
+        // start_{d+1}) with lo + d: short runs by one thread, longer runs by
+        // a warp (listed), so no bucket size is limited by the item array.
+        auto put = [&](int j, u32 d) {
+          const Key v = lo + (Key)d;
+          if constexpr (DT == DT_F64) {
+            reinterpret_cast<u64 *>(g)[j] = key_to_f64(v);
+          } else {
+            reinterpret_cast<Item *>(g)[j] = (Item)v;
+          }
+        };
+        for (int d = tid; d < nd; d += NT) {
+          const int st = (int)s_end[d], en = d + 1 < nd ? (int)s_end[d + 1] : m;
+          if (en - st > 32) {
+            const u32 slot = atomicAdd(&s_nbig, 1u);
+            if (slot < BIGCAP) {
+              s_big[slot] = (u32)d;
+              continue;
+            }
+          }
+          for (int j = st; j < en; ++j) put(j, (u32)d);
+        }
+        __syncthreads();
+        const int nl = min((int)s_nbig, BIGCAP);
+        for (int q = wid; q < nl; q += NT / 32) {
+          const u32 d = s_big[q];
+          const int st = (int)s_end[d], en = (int)d + 1 < nd ? (int)s_end[d + 1] : m;
+          for (int j = st + lane; j < en; j += 32) put(j, d);
+        }
+        __syncthreads();
+        continue;
+      }
+    }
     // split point of an oversized bucket (see BaseSplitArgs)
     int dsplit = nd, mA = m;
     if (SPLITK && BI::SPLIT && m > (int)sp.cap) {

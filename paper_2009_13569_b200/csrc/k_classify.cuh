@@ -263,30 +263,6 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
 
 namespace ips4o {
 
-// ------------------------------------------------------------------ K2, 8/16-byte elements
-// Same algorithm as classify_kernel, with the tile held in registers: each
-// thread owns RT_IPT elements of the tile (coalesced loads, the next tile is
-// prefetched into registers while the current one is classified), the tile
-// elements of emitted blocks are scattered into a shared staging array in
-// bucket order, and a block -> bucket map replaces per-block searches.
-template <int DT> struct ClsReg {
-  using Tr = Traits<DT>;
-  static constexpr int NT = 512;
-  static constexpr int T = Tr::D == 8 ? 4096 : 2048;
-  static constexpr int IPT = T / NT;
-  static constexpr int D = Tr::D, B = Tr::B, KI = Tr::KIDX;
-  static constexpr int MAXBLK = T / B + KI;
-  static constexpr size_t off_buf = 0;
-  static constexpr size_t off_stage = off_buf + (size_t)KI * B * D;
-  static constexpr size_t off_tree = off_stage + (size_t)T * D;
-  static constexpr size_t off_u32 = off_tree + 2 * KI * sizeof(typename Tr::Key);
-  // u32 arrays: fill, tcnt, cnt, boff, eoff, nb (KI each) + ws (NT/32 + 1)
-  static constexpr size_t off_blkb = off_u32 + (6 * KI + NT / 32 + 1) * 4;
-  static constexpr int LUT_BITS = 11;
-  static constexpr size_t off_lut = (off_blkb + (size_t)MAXBLK * 2 + 15) / 16 * 16;
-  static constexpr size_t bytes = off_lut + ((size_t)4 << LUT_BITS);
-};
-
 template <int DT>
 __device__ __forceinline__ typename Traits<DT>::Key elem_key(const typename Traits<DT>::Unit &x) {
   if constexpr (DT == DT_PAIR) {
@@ -300,293 +276,11 @@ __device__ __forceinline__ typename Traits<DT>::Key elem_key(const typename Trai
   }
 }
 
-template <int DT, int ALGO>
-__global__ void __launch_bounds__(ClsReg<DT>::NT, 1) classify_reg_kernel(LevelArgs A) {
-  using Tr = Traits<DT>;
-  using Key = typename Tr::Key;
-  using Unit = typename Tr::Unit;  // one element
-  using S = ClsReg<DT>;
-  constexpr int NT = S::NT, T = S::T, IPT = S::IPT, B = Tr::B, KI = Tr::KIDX;
-  constexpr int NWARPS = NT / 32;
-  static_assert(Tr::D == sizeof(Unit), "one unit per element");
-  static_assert(KI <= NT, "one thread per bucket in the scans");
-
-  extern __shared__ __align__(16) char smem[];
-  Unit *s_buf = reinterpret_cast<Unit *>(smem + S::off_buf);
-  Unit *s_stage = reinterpret_cast<Unit *>(smem + S::off_stage);
-  Key *s_tree = reinterpret_cast<Key *>(smem + S::off_tree);
-  Key *s_spl = s_tree + KI;
-  u32 *s_fill = reinterpret_cast<u32 *>(smem + S::off_u32);
-  u32 *s_tcnt = s_fill + KI;
-  u32 *s_cnt = s_tcnt + KI;
-  u32 *s_boff = s_cnt + KI;
-  u32 *s_eoff = s_boff + KI;
-  u32 *s_nb = s_eoff + KI;
-  u32 *s_ws = s_nb + KI;
-  u64 *s_plan = reinterpret_cast<u64 *>(s_eoff);  // KI words over s_eoff/s_nb
-  unsigned short *s_blkb = reinterpret_cast<unsigned short *>(smem + S::off_blkb);
-  u32 *s_lut = reinterpret_cast<u32 *>(smem + S::off_lut);
-
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const u32 stripe = blockIdx.x;
-  const u32 ti = A.stripe_task[stripe];
-  const LevelTask &L = A.tasks[ti];
-  const int K = (int)L.K, l = (int)L.l, eq = (int)L.equality, shift = L.shift;
-  const u32 dmask = L.K - 1;
-  const u64 size = L.t.size;
-  const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
-  const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
-  Unit *gtask = reinterpret_cast<Unit *>(A.base + L.t.begin * (u64)Tr::D);
-
-  if (ALGO == ALGO_TREE) {
-    const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
-    for (int i = tid; i < (1 << l); i += NT) {
-      s_tree[i] = gt[i];
-      s_spl[i] = gt[KI + i];
-    }
-  }
-  for (int j = tid; j < KI; j += NT) {
-    s_tcnt[j] = 0;
-    s_cnt[j] = 0;
-    s_fill[j] = 0;
-  }
-  u32 myfill = 0;  // buffered elements of bucket tid (tid < KI)
-
-  // Lookup table of starting leaves addressed by the most significant bits of
-  // (key - llo), over the sample's key range [llo, lhi] inside
-  // the task bounds [tlo, thi]: slot q covers [llo + q*2^ls, llo + (q+1)*2^ls)
-  // (slot 0 extends down to tlo, the last slot up to thi) and stores the
-  // leaves of its first and last key; the search is then only needed between
-  // those leaves.  Exact: leaf = #{splitters < key}.
-  const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
-  Key llo = tlo, lhi = thi;
-  if (ALGO == ALGO_TREE) {
-    llo = key_from_words<Key>(L.lut_lo);
-    lhi = key_from_words<Key>(L.lut_hi);
-    if (llo < tlo) llo = tlo;
-    if (lhi > thi) lhi = thi;
-    if (lhi < llo) lhi = llo;
-  }
-  int ls = bitlen((Key)(lhi - llo)) - S::LUT_BITS;
-  if (ls < 0) ls = 0;
-  const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
-  const int nspl = (1 << l) - 1;  // s
-  if (ALGO == ALGO_TREE) {
-    __syncthreads();
-    auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
-      u32 a = 0, b = (u32)nspl;
-      while (a < b) {
-        u32 mid = (a + b) >> 1;
-        if (s_spl[mid] < v) a = mid + 1;
-        else b = mid;
-      }
-      return a;
-    };
-    for (u32 q = tid; q < (1u << S::LUT_BITS); q += NT) {
-      u32 e = 0;
-      if (q < nlut_used) {
-        const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
-        const Key r1 = q + 1 == nlut_used ? thi : llo + (((Key)(q + 1)) << ls) - 1;
-        const u32 a = lower(r0), b = lower(r1);
-        e = a | ((b - a) << 16);
-      }
-      s_lut[q] = e;
-    }
-  }
-  const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
-  Key kmin = key_max<Key>(), kmax = (Key)0;
-
-  const u64 n = s1 > s0 ? s1 - s0 : 0;
-  const u64 ntiles = (n + T - 1) / T;
-  u64 front = 0;
-  Unit x[IPT], y[IPT];
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    u64 i = s0 + tid + (u64)k * NT;
-    if (i < s1) x[k] = gtask[i];
-  }
-  __syncthreads();
-
-  for (u64 t = 0; t < ntiles; ++t) {
-    const u64 e0 = s0 + t * T;
-    const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
-    // the tile after next streams into L2; the next tile goes into registers
-    if (t + 2 < ntiles) {
-      const u64 p0 = e0 + 2 * (u64)T;
-      const u64 p1 = p0 + T < s1 ? p0 + T : s1;
-      prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), tid, 2);
-    }
-    if (t + 1 < ntiles) {
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) {
-        u64 i = e0 + T + tid + (u64)k * NT;
-        if (i < s1) y[k] = gtask[i];
-      }
-    }
-    // ---- classify (Alg. 1 batched over IPT elements)
-    u32 bkt[IPT], rank[IPT];
-    {
-      Key key[IPT];
-#pragma unroll
-      for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
-      if (want_minmax) {
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          if (tid + k * NT < cnt) {
-            kmin = key[k] < kmin ? key[k] : kmin;
-            kmax = key[k] > kmax ? key[k] : kmax;
-          }
-        }
-      }
-      if (ALGO == ALGO_TREE) {
-        u32 ent[IPT];
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          const Key dk = key[k] - llo;
-          u32 q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
-          ent[k] = s_lut[q];
-        }
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          u32 a = ent[k] & 0xFFFFu, b = a + (ent[k] >> 16);
-          while (a < b) {  // lower bound inside the slot's leaf interval
-            u32 mid = (a + b) >> 1;
-            if (s_spl[mid] < key[k]) a = mid + 1;
-            else b = mid;
-          }
-          bkt[k] = eq ? 2 * a + 1 - (key[k] < s_spl[a] ? 1u : 0u) : a;
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) rank[k] = (tid + k * NT < cnt) ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;
-    __syncthreads();
-
-    // ---- per-bucket plan: blocks to emit (nb) and tile elements they take
-    // (em); exclusive scan of (nb << 16 | em) with one barrier (each warp
-    // adds up the totals of the warps before it)
-    u32 tc = 0, tot = 0, nb = 0, em = 0;
-    if (tid < KI) {
-      tc = s_tcnt[tid];
-      s_tcnt[tid] = 0;
-      tot = myfill + tc;
-      nb = tot / B;
-      em = nb ? nb * B - myfill : 0;
-    }
-    const u32 pv = (nb << 16) | em;
-    u32 incl = pv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      u32 yv = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += yv;
-    }
-    if (lane == 31) s_ws[wid] = incl;
-    __syncthreads();
-    const u32 wv = lane < NWARPS ? s_ws[lane] : 0;
-    const u32 wpre = __reduce_add_sync(0xffffffffu, lane < wid ? wv : 0u);
-    const u32 total = __reduce_add_sync(0xffffffffu, wv);
-    if (tid < KI) {
-      const u32 pre = wpre + incl - pv;
-      const u32 bo = pre >> 16;
-      s_boff[tid] = bo;
-      // plan word: fill | cut << 16 | eoff << 32
-      s_plan[tid] = (u64)myfill | ((u64)(nb * B) << 16) | ((u64)(pre & 0xFFFFu) << 32);
-      s_cnt[tid] += tc;
-      for (u32 q = 0; q < nb; ++q) s_blkb[bo + q] = (unsigned short)tid;
-      myfill = tot - nb * B;
-    }
-    const u32 nblocks = total >> 16;
-    __syncthreads();
-
-    // ---- scatter the tile elements of emitted blocks in bucket order; the
-    //      others remember their buffer slot
-    u32 slot[IPT];
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      slot[k] = 0xFFFFFFFFu;
-      if (tid + k * NT < cnt) {
-        const u32 j = bkt[k];
-        const u64 pl = s_plan[j];
-        const u32 v = (u32)(pl & 0xFFFFu) + rank[k];
-        const u32 cut = (u32)(pl >> 16) & 0xFFFFu;
-        if (v < cut) s_stage[(u32)(pl >> 32) + rank[k]] = x[k];
-        else slot[k] = j * B + (v - cut);
-      }
-    }
-    __syncthreads();
-
-    // ---- emit full blocks to the stripe's write front (coalesced per warp)
-    for (u32 g = wid; g < nblocks; g += NWARPS) {
-      const u32 j = s_blkb[g];
-      const u32 q = g - s_boff[j];
-      const u64 pl = s_plan[j];
-      const u32 bf = (u32)(pl & 0xFFFFu);
-      const u32 eo = (u32)(pl >> 32);
-      Unit *dst = gtask + s0 + (front + g) * B;
-      if (lane == 0) A.bid[L.blk_off + s0 / B + front + g] = (unsigned short)j;
-#pragma unroll
-      for (int e = lane; e < B; e += 32) {
-        const u32 v = q * B + e;
-        dst[e] = v < bf ? s_buf[j * B + v] : s_stage[eo + v - bf];
-      }
-    }
-    front += nblocks;
-    __syncthreads();
-
-    // ---- remaining tile elements go to the (now free) buffer slots.  No
-    //      barrier needed before the next tile: its first shared write that
-    //      conflicts (emission reading s_buf) comes after its barriers.
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) {
-      if (slot[k] != 0xFFFFFFFFu) s_buf[slot[k]] = x[k];
-    }
-#pragma unroll
-    for (int k = 0; k < IPT; ++k) x[k] = y[k];
-  }
-
-  // ---- outputs: counts, partial fill, full blocks, partial buffers
-  if (tid < KI) s_fill[tid] = myfill;
-  __syncthreads();
-  const u64 sbase = L.sbk_off + (u64)(stripe - L.stripe_first) * L.kidx;
-  for (int j = tid; j < (int)L.kidx; j += NT) {
-    A.counts[sbase + j] = s_cnt[j];
-    A.pfill[sbase + j] = s_fill[j];
-  }
-  if (tid == 0) A.fullblocks[stripe] = (u32)front;
-  for (int j = wid; j < K; j += NWARPS) {
-    const int f = (int)s_fill[j];
-    Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * Tr::D);
-    for (int u = lane; u < f; u += 32) dst[u] = s_buf[j * B + u];
-  }
-  if constexpr (sizeof(Key) == 8) {
-    if (want_minmax) {
-      // key range of the task, replacing the skipped pre-pass (TF_MINMAX)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        Key a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
-        kmin = a < kmin ? a : kmin;
-        kmax = b > kmax ? b : kmax;
-      }
-      if (lane == 0) {
-        atomicMin(reinterpret_cast<unsigned long long *>(&A.minmax[0]), (unsigned long long)kmin);
-        atomicMax(reinterpret_cast<unsigned long long *>(&A.minmax[1]), (unsigned long long)kmax);
-      }
-    }
-  }
-}
-
-}  // namespace ips4o
-
-namespace ips4o {
-
 // ------------------------------------------------------------------ K2 v2, 8/16-byte elements
 // Tile-synchronous classification with block buffers, three barriers per tile.
 // 1024 threads; each owns IPT elements of a T-element tile in registers (the
 // next tile is loaded while the current one is processed).  Per tile:
-//   classify (LUT of starting leaves + short search, P:4052-4053) and rank by
+//   classify (LUT of starting leaves + short search, P:4049-4050) and rank by
 //   shared atomics  | A |  the previous tile's leftovers enter the freed
 //   buffers; one scan over the k' buckets plans, per bucket j, nb_j full
 //   blocks: block 0 is buffer j completed by the first B - fill_j tile

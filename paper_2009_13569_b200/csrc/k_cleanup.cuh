@@ -2,6 +2,7 @@
 // (Alg. 2, adapted to device task lists).
 #pragma once
 #include "common.cuh"
+#include "k_basecase.cuh"
 #include "k_classify.cuh"
 
 namespace ips4o {
@@ -201,8 +202,10 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
       u32 slot = atomicAdd(&A.counters[1], 1u);
       if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;
       atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
-    } else if (sz <= A.base_split_elems) {
-      // up to twice the capacity: the base case's two-pass split (K7s)
+    } else if (sz <= A.base_split_elems ||
+               (BaseItem<DT>::KEY_ONLY && sz <= 65535 && hi - lo < (Key)basecase_count_range<DT>())) {
+      // up to twice the capacity: the base case's two-pass split (K7s); a
+      // narrow key range of a key-only type: counted exactly (any size)
       u32 slot = atomicAdd(&A.counters[8], 1u);
       if (slot < A.base_cap_tasks) A.split_tasks[slot] = c;
       atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);

@@ -252,6 +252,25 @@ def test_digit_sparse_keys_measured(ips, orc, dtype):
     assert st["levels"] <= 3, st["tasks_per_level"]
 
 
+@pytest.mark.parametrize("dtype", [U64, F64, U32])
+@pytest.mark.parametrize("nvals", [5000, 40000])
+def test_narrow_range_counting_base_case(ips, orc, dtype, nvals):
+    """Key-only buckets whose key range is narrow are counted exactly in the
+    base case whatever their size (K6 sends them there, K7 writes them from
+    the counts); with base_cap=1000 most level-1 buckets exceed 2M."""
+    n = (1 << 20) + 11
+    rng = np.random.default_rng(nvals)
+    v = rng.integers(0, nvals, n)
+    if dtype == U64:
+        a = (v.astype(np.uint64) + np.uint64(3 << 40))
+    elif dtype == U32:
+        a = (v + 123456).astype(np.uint32)
+    else:
+        a = (v.astype(np.float64) - nvals / 2) * 0.25  # exact binary fractions, negatives
+    g, st = gpu_sort(a, dtype, base_cap=1000)
+    check(orc, a, g, dtype)
+
+
 def _patterns(n, rng):
     m = np.uint64(2**64 - 1)
     u = gen.uniform_u64(n, 77)
