@@ -339,9 +339,9 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       if (!direct && ds == 0 && r32 < (1u << BI::DBMAX)) {
         direct = true;  // the static area holds the r32 + 1 counters
       } else if (!direct && ds == 0) {
-        // (key-only items are then written from the counts alone: no item
-        // array at all)
-        const u64 used = BI::KEY_ONLY ? 0 : (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
+        // (key-only buckets larger than the item array are then written from
+        // the counts alone: no item array at all)
+        const u64 used = BI::KEY_ONLY && mm > BI::CAP ? 0 : (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
         const u64 hb = (((u64)r32 / 2 + 1) * 4 + 15) & ~15ull;  // bytes for r32 + 1 counters
         const u64 hend = S::off_hist + (u64)HSTAT * 4;
         if (hend >= hb && hend - hb >= S::off_items + used) {
@@ -512,11 +512,14 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     BC_PHASE(2)
     const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);  // starts, ends after the scatter
     if constexpr (BI::KEY_ONLY) {
-      if (exact) {
+      if (exact && m > BI::CAP) {
         // One key value per digit and nothing but the key in an item: the
-        // counts alone are the sorted bucket.  Digit d fills [start_d,
-        // start_{d+1}) with lo + d: short runs by one thread, longer runs by
-        // a warp (listed), so no bucket size is limited by the item array.
+        // counts alone are the sorted bucket (the bucket size is then not
+        // limited by the item array; buckets that fit take the scatter below).
+        // Position j holds lo + d for the largest d with start_d <= j: a warp
+        // takes 32 consecutive positions (coalesced stores), two lanes bound
+        // the digits of its first and last position by binary search over
+        // all starts, and each lane searches between those bounds.
         auto put = [&](int j, u32 d) {
           const Key v = lo + (Key)d;
           if constexpr (DT == DT_F64) {
@@ -525,23 +528,20 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             reinterpret_cast<Item *>(g)[j] = (Item)v;
           }
         };
-        for (int d = tid; d < nd; d += NT) {
-          const int st = (int)s_end[d], en = d + 1 < nd ? (int)s_end[d + 1] : m;
-          if (en - st > 32) {
-            const u32 slot = atomicAdd(&s_nbig, 1u);
-            if (slot < BIGCAP) {
-              s_big[slot] = (u32)d;
-              continue;
-            }
+        auto last_start_le = [&](int j, u32 a, u32 b) -> u32 {  // in [a, b]
+          while (a < b) {
+            const u32 mid = (a + b + 1) >> 1;
+            if ((int)s_end[mid] <= j) a = mid;
+            else b = mid - 1;
           }
-          for (int j = st; j < en; ++j) put(j, (u32)d);
-        }
-        __syncthreads();
-        const int nl = min((int)s_nbig, BIGCAP);
-        for (int q = wid; q < nl; q += NT / 32) {
-          const u32 d = s_big[q];
-          const int st = (int)s_end[d], en = (int)d + 1 < nd ? (int)s_end[d + 1] : m;
-          for (int j = st + lane; j < en; j += 32) put(j, d);
+          return a;
+        };
+        for (int sg = wid; sg * 32 < m; sg += NT / 32) {
+          const int j = sg * 32 + lane;
+          u32 bd = 0;
+          if (lane < 2) bd = last_start_le(lane == 0 ? sg * 32 : min(sg * 32 + 31, m - 1), 0u, (u32)nd - 1);
+          const u32 da = __shfl_sync(0xffffffffu, bd, 0), db = __shfl_sync(0xffffffffu, bd, 1);
+          if (j < m) put(j, last_start_le(j, da, db));
         }
         __syncthreads();
         continue;
