@@ -266,7 +266,9 @@ def test_narrow_range_counting_base_case(ips, orc, dtype, nvals):
     elif dtype == U32:
         a = (v + 123456).astype(np.uint32)
     else:
-        a = (v.astype(np.float64) - nvals / 2) * 0.25  # exact binary fractions, negatives
+        # consecutive doubles (adjacent order-preserving keys) on both sides of 0
+        ulp = np.float64(2.0**-52)
+        a = np.where(v % 2 == 0, 1.0 + (v // 2) * ulp, -(1.0 + (v // 2) * ulp)).astype(np.float64)
     g, st = gpu_sort(a, dtype, base_cap=1000)
     check(orc, a, g, dtype)
 
