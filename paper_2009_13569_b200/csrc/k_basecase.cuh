@@ -445,17 +445,28 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     //    [t*WPT, (t+1)*WPT) (vector loads), one block-wide scan of the thread
     //    totals.  Each word becomes (start(2w), start(2w+1)).
     if (hbig) {
-      // exact counters (no long runs): contiguous words per thread, two passes
-      const int wpt = (nw + NT - 1) / NT;
-      const int w0 = min(tid * wpt, nw), w1 = min(w0 + wpt, nw);
-      u32 tot = 0;
-      for (int w = w0; w < w1; ++w) tot += (s_hist[w] & 0xFFFFu) + (s_hist[w] >> 16);
+      // exact counters (no long runs): warp wi scans the word segment
+      // [wi*seg, (wi+1)*seg) row by row (lane l reads word row + l: no bank
+      // conflicts), after a block scan of the warp totals
+      const int seg = ((nw + NT / 32 - 1) / (NT / 32) + 31) & ~31;
+      const int s0 = min(wid * seg, nw), s1 = min(s0 + seg, nw);
+      u32 wtot = 0;
+      for (int w = s0 + lane; w < s1; w += 32) wtot += (s_hist[w] & 0xFFFFu) + (s_hist[w] >> 16);
+      wtot = __reduce_add_sync(0xffffffffu, wtot);
       u32 all;
-      u32 st = block_exclusive_scan<NT>(tot, s_ws, &all);
-      for (int w = w0; w < w1; ++w) {
-        const u32 h = s_hist[w], c0 = h & 0xFFFFu, c1 = h >> 16;
-        s_hist[w] = st | ((st + c0) << 16);
-        st += c0 + c1;
+      u32 carry = __shfl_sync(0xffffffffu, block_exclusive_scan<NT>(lane == 0 ? wtot : 0u, s_ws, &all), 0);
+      for (int row = s0; row < s1; row += 32) {
+        const int w = row + lane;
+        const u32 h = w < s1 ? s_hist[w] : 0u, c0 = h & 0xFFFFu, t = c0 + (h >> 16);
+        u32 x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const u32 st = carry + x - t;
+        if (w < s1) s_hist[w] = st | ((st + c0) << 16);
+        carry += __shfl_sync(0xffffffffu, x, 31);
       }
     } else {
       constexpr int WPT = ((1 << BI::DBMAX) / 2 + NT - 1) / NT;
