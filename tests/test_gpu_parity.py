@@ -372,12 +372,17 @@ def test_rec100_extras(ips, orc):
         check(orc, r, g, REC100)
 
 
-def test_scratch_is_reported_and_bounded(ips, orc):
-    n = 1 << 21
-    a = gen.uniform_u64(n, 2)
-    g, st = gpu_sort(a, U64)
-    assert 0 < st["scratch_bytes"] <= ips.scratch_bytes(n, U64)
-    check(orc, a, g, U64)
+@pytest.mark.parametrize("dtype", [U64, U32, PAIR, QUARTET])
+@pytest.mark.parametrize("algo", ["tree", "digit"])
+@pytest.mark.parametrize("base_cap", [0, 500])
+def test_scratch_is_reported_and_bounded(ips, orc, dtype, algo, base_cap):
+    """The peak scratch of a sort never exceeds ips4o_scratch_bytes (deep
+    recursion, split base cases, K0m measurement of IPS2Ra included)."""
+    n = (1 << 21) + 5
+    a = make(dtype, n, 2, "uniform")
+    g, st = gpu_sort(a, dtype, base_cap=base_cap, algo=ips.DIGIT if algo == "digit" else ips.TREE)
+    assert 0 < st["scratch_bytes"] <= ips.scratch_bytes(n, dtype, base_cap=base_cap), st["scratch_bytes"]
+    check(orc, a, g, dtype)
 
 
 def test_sort_host_end_to_end(ips, orc):
