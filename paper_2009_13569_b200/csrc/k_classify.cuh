@@ -290,6 +290,9 @@ __device__ __forceinline__ typename Traits<DT>::Key elem_key(const typename Trai
 //   registers as a leftover  | C |  warps copy the emitted blocks to the
 //   stripe's write front.  Leftovers are written into buffer j
 //   after the next tile's barrier A, once the copies have read buffer j.
+#ifndef IPS4O_CLS_PF
+#define IPS4O_CLS_PF 2  // L2 prefetch distance in tiles
+#endif
 template <int DT> struct ClsV2 {
   using Tr = Traits<DT>;
   using Key = typename Tr::Key;
@@ -437,8 +440,8 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   for (u64 t = 0; t < ntiles; ++t) {
     const u64 e0 = s0 + t * T;
     const int cnt = (int)((s1 - e0) < (u64)T ? (s1 - e0) : (u64)T);
-    if (wid == 0 && t + 2 < ntiles) {
-      const u64 p0 = e0 + 2 * (u64)T;
+    if (wid == 0 && t + IPS4O_CLS_PF < ntiles) {
+      const u64 p0 = e0 + IPS4O_CLS_PF * (u64)T;
       const u64 p1 = p0 + T < s1 ? p0 + T : s1;
       prefetch_l2(gtask + p0, (p1 - p0) * sizeof(Unit), lane, 2);
     }
