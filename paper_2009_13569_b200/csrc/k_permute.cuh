@@ -207,7 +207,10 @@ constexpr int PERM_WARPS = 8;
 #ifndef IPS4O_PERM_MINB
 #define IPS4O_PERM_MINB 8  // full occupancy: 32 registers (a few bytes spill)
 #endif
-constexpr u32 PERM_HOP_WINDOW = 64;  // tasks an idle agent may look ahead
+#ifndef IPS4O_PERM_HOP_WINDOW
+#define IPS4O_PERM_HOP_WINDOW 64
+#endif
+constexpr u32 PERM_HOP_WINDOW = IPS4O_PERM_HOP_WINDOW;  // tasks an idle agent may look ahead
 #ifndef IPS4O_PERM_TREE_PACE_NS
 #define IPS4O_PERM_TREE_PACE_NS 0
 #endif
