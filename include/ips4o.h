@@ -193,7 +193,10 @@ int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream,
  * P:432-437 built from the u sorted, unique splitter keys at HOST pointer
  * splitters (raw key form, key_bytes each); equality buckets if `equality`.
  * Writes one uint32 bucket index per element to DEVICE pointer out.  This is
- * the classifier the classification kernel uses (test hook).  Synchronous. */
+ * the device tree walk (Alg. 1) that the record/quartet classifier runs and
+ * that the 4/8/16-byte classifier's lookup table of starting leaves
+ * must agree with -- parity of whole partition steps checks the
+ * latter (test hook).  Synchronous. */
 int ips4o_classify(const void *elems, uint64_t n, int dtype, const void *splitters,
                    int u, int equality, uint32_t *out, void *stream);
 
