@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
 // so an agent learns where a swapped-out block goes from a 2-byte load that
 // returns long before the block, and issues the next atomic while the block
 // is still in flight.
-constexpr int PERM_WARPS = 8;
+#ifndef IPS4O_PERM_WARPS
+#define IPS4O_PERM_WARPS 8
+#endif
+constexpr int PERM_WARPS = IPS4O_PERM_WARPS;
 #ifndef IPS4O_PERM_MINB
 #define IPS4O_PERM_MINB 8  // full occupancy: 32 registers (a few bytes spill)
 #endif
