@@ -460,3 +460,77 @@ def test_sample_tree_subroracle_is_consistent(orc):
     for x in a[:500]:
         assert orc.classify_tree(st["tree"], st["splitter"], st["l"], st["equality"], U64,
                                  np.array([x])) == _py_bucket(padded, int(x), st["equality"])
+
+
+# ----------------------------------------------------------------- R8 pin
+M64 = (1 << 64) - 1
+
+
+def _py_mix(z):
+    """SplitMix64 finaliser (Steele, Lea, Flood), written out with Python ints."""
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _py_sample_index(seed, level, begin, size, j):
+    """DESIGN R8 transcribed independently of oracle.c:
+    base = mix(seed + g(level+1)) ^ mix(begin + g(size+1)), u_j = mix(base + g(j+1)),
+    index = begin + floor(u_j * size / 2^64)."""
+    g = 0x9E3779B97F4A7C15
+    base = _py_mix((seed + g * (level + 1)) & M64) ^ _py_mix((begin + g * (size + 1)) & M64)
+    u = _py_mix((base + g * (j + 1)) & M64)
+    return begin + ((u * size) >> 64)
+
+
+def test_sample_index_matches_r8_transcription(orc):
+    """orc_sample_index equals an independent Python transcription of R8 on
+    every argument corner (large seeds, levels, 2^32-sized tasks, j wrap)."""
+    cases = [(0, 0, 0, 1, 0), (1, 0, 0, 2, 0), (42, 0, 0, 1 << 30, 5), (0x1F4A2C7, 1, 123456, 4194304, 16383),
+             (M64, 7, (1 << 40) + 3, (1 << 32) - 1, (1 << 20) + 1), (5, 1, 1000, 97, 3), (5, 2, 1000, 97, 3)]
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        cases.append((int(rng.integers(0, 1 << 63)) * 2 + 1, int(rng.integers(0, 64)), int(rng.integers(0, 1 << 40)),
+                      int(rng.integers(1, 1 << 34)), int(rng.integers(0, 1 << 20))))
+    for c in cases:
+        assert orc.sample_index(*c) == _py_sample_index(*c), c
+
+
+# ----------------------------------------------------------------- checkers reject
+@pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
+def test_multiset_hash_and_is_sorted_reject_changes(orc, dtype):
+    """The invariant checkers are not vacuous: a changed byte changes the
+    multiset hash, a swapped pair of distinct keys is not sorted, and the
+    parity checker reports the first differing element."""
+    D = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}[dtype]
+    rng = np.random.default_rng(dtype + 3)
+    n = 257
+    a = rng.integers(0, 256, n * D, dtype=np.uint8)
+    if dtype == F64:  # finite, non-negative doubles (no NaN / -0.0, R2)
+        a = rng.random(n).view(np.uint8)
+    s = orc.sort(a, dtype)
+    assert orc.is_sorted(s, dtype)
+    h = orc.multiset_hash(a, dtype)
+    assert orc.multiset_hash(s, dtype) == h
+    for pos in [0, D - 1, 17 * D + 3, n * D - 1]:
+        b = a.copy()
+        b[pos] ^= 0x10
+        assert orc.multiset_hash(b, dtype) != h, pos
+    # a record duplicated over another changes the multiset
+    b = a.copy()
+    b[5 * D:6 * D] = b[9 * D:10 * D]
+    assert orc.multiset_hash(b, dtype) != h
+    # swap two adjacent elements of the sorted output with distinct keys
+    E = s.reshape(n, D).copy()
+    for i in range(n - 1):
+        if orc.less(dtype, E[i], E[i + 1]):
+            E[[i, i + 1]] = E[[i + 1, i]]
+            break
+    bad = E.reshape(-1)
+    assert not orc.is_sorted(bad, dtype)
+    assert orc.parity(bad, s, dtype) == i
+    # a payload change inside an equal-key run is a multiset error for parity
+    if dtype in (PAIR, REC100, QUARTET):
+        P = s.reshape(n, D).copy()
+        P[n // 2, D - 1] ^= 1
+        assert orc.parity(P.reshape(-1), s, dtype) != -1
