@@ -34,7 +34,7 @@ FULLSIZE_JOBS = [
     ("exponential_f64", 1 << 28, 2),   # c2
     ("uniform_u32", 1 << 28, 6),       # NEXT-2
 ]
-MAX_CONCURRENT = int(os.environ.get("IPS4O_ORACLE_JOBS", "4"))
+MAX_CONCURRENT = int(os.environ.get("IPS4O_ORACLE_JOBS", "7"))
 
 
 def job_key(name: str, n: int, seed: int) -> str:
