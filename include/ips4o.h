@@ -63,10 +63,12 @@ enum ips4o_algo {
 enum ips4o_status {
     IPS4O_OK = 0,
     IPS4O_ERR_INVALID = -1, /* NULL ptr with n > 0, unknown dtype/algo, misaligned
-                               ptr (needs 16-byte alignment), n >= 2^32, bad option */
+                               ptr (4 B for U32, 8 B for U64/F64, 16 B otherwise),
+                               n >= 2^32, bad option                               */
     IPS4O_ERR_NOMEM = -2,   /* device scratch (or pinned host) allocation failed  */
-    IPS4O_ERR_CUDA = -3,    /* a CUDA launch or runtime call failed; the CUDA error
-                               string is kept for ips4o_status_string()           */
+    IPS4O_ERR_CUDA = -3,    /* a CUDA launch or runtime call failed, or (calls that
+                               synchronise) the device reported an error flag; the
+                               text is kept for ips4o_status_string()              */
     IPS4O_ERR_NOGPU = -4    /* no CUDA device / device is not sm_100             */
 };
 
@@ -74,7 +76,8 @@ enum ips4o_status {
 typedef struct ips4o_options {
     int32_t algo;          /* enum ips4o_algo (default TREE)                          */
     int32_t k_max;         /* max leaves/digits per partitioning step (k=256),
-                              power of two in [2, 256]; default per dtype            */
+                              power of two in [2, 256] ([4, 256] for TREE: >= 3
+                              splitters guarantee progress); default per dtype       */
     uint64_t seed;         /* sampling seed (DESIGN R8); default 0x1F4A2C7            */
     int32_t alpha_min;     /* lower bound of the oversampling factor alpha; the paper
                               uses alpha = 0.2 log2 n, default max(that, 64) */
@@ -86,7 +89,8 @@ typedef struct ips4o_options {
     int32_t skip_prepass;  /* 1 = do not run the easy-input pre-pass   */
     int32_t skip_basecase; /* 1 = do not run the base case (debug; leaves buckets
                               unsorted)                                               */
-    int32_t timing;        /* 1 = record per-kernel device times into ips4o_stats     */
+    int32_t timing;        /* 1 = record per-kernel device times into ips4o_stats
+                              (device globaltimer stamps per kernel; needs `out`)    */
     int32_t reserved[7];
 } ips4o_options;
 
@@ -96,8 +100,9 @@ typedef struct ips4o_options {
 /* Statistics (optional output of ips4o_sort_ex; a non-NULL pointer implies a
  * stream synchronisation before return). */
 typedef struct ips4o_stats {
-    uint64_t scratch_bytes;           /* peak device scratch of this call             */
-    int32_t levels;                   /* partitioning levels executed                 */
+    uint64_t scratch_bytes;           /* device scratch allocated by this call        */
+    int32_t levels;                   /* partitioning rounds executed (= levels unless
+                                         the arena deferred tasks to a later round)   */
     int32_t easy_input;               /* 0 none, 1 sorted, 2 reverse-sorted (reversed),
                                          3 all keys equal                             */
     uint64_t tasks_per_level[IPS4O_MAX_LEVELS_REPORTED];
@@ -105,28 +110,41 @@ typedef struct ips4o_stats {
     uint64_t basecase_tasks;          /* number of one-CTA base-case sorts            */
     uint64_t basecase_elems;          /* elements sorted by the base case             */
     uint64_t equal_elems;             /* elements left in terminal equality buckets   */
-    float kernel_ms[IPS4O_NUM_KERNELS]; /* per kernel family, when opt->timing:
-                                         0 prepass, 1 sample, 2 classify, 3 boundaries,
-                                         4 stripe-fix, 5 permute, 6 cleanup, 7 schedule,
-                                         8 base case, 9 reverse, 10 host planning (wall),
-                                         11 total (device)                            */
-    uint64_t kernel_launches;         /* kernels launched by this call                */
+    float kernel_ms[IPS4O_NUM_KERNELS]; /* per kernel family, when opt->timing, summed
+                                         over launches (earliest CTA start to latest
+                                         warp end, device globaltimer):
+                                         0 prepass (+ entry), 1 sample (+ IPS2Ra range
+                                         measure), 2 classify, 3 boundaries + schedule,
+                                         4 stripe-fix, 5 permute, 6 cleanup, 7 unused
+                                         (the scheduler runs inside 3), 8 base case,
+                                         9 reverse, 10 device planner, 11 total device
+                                         time of the sort (first start to last end)   */
+    uint64_t kernel_launches;         /* kernels launched by this call (1 by the host,
+                                         the rest by the device planner)              */
 } ips4o_stats;
 
 /* Sort the n elements at DEVICE pointer ptr ascending, in place, unstably,
  * stream-ordered on `stream` (a cudaStream_t, or NULL for the legacy default
- * stream).  ptr must be 16-byte aligned (torch's allocator gives >= 256 B).
- * The caller owns ptr and keeps it alive until the stream work completes.
- * Scratch is allocated stream-ordered from the device's default memory pool
- * and released before return.  The call synchronises `stream` once per
- * partitioning level to read back the task list (DESIGN "Host loop"); from
- * the caller's point of view it behaves like a blocking library call whose
- * results are visible to later work on `stream`.
- * Errors: IPS4O_ERR_INVALID, IPS4O_ERR_NOMEM, IPS4O_ERR_CUDA, IPS4O_ERR_NOGPU.
+ * stream).  ptr alignment: 4 B (U32), 8 B (U64, F64), 16 B (PAIR, REC100,
+ * QUARTET).  The caller owns ptr and keeps it alive until the stream work
+ * completes.
+ * Asynchronous like a kernel launch: the call enqueues a stream-ordered
+ * scratch allocation (from a memory pool the library owns per device), ONE
+ * kernel, and the scratch free, and returns; every partitioning level is
+ * planned and launched by the device (recursion on the device, P:1119-1163,
+ * DESIGN "Device planner").  The enqueued work can be captured into a CUDA
+ * graph (stream capture) once the device has been initialised by an earlier
+ * call (the first call per device creates the pool and a status word).
+ * Errors: IPS4O_ERR_INVALID, IPS4O_ERR_NOMEM, IPS4O_ERR_CUDA, IPS4O_ERR_NOGPU
+ * are returned for what the host can see; an error the device detects later
+ * (an internal invariant) is ORed into the device's status word
+ * (ips4o_device_status) and reported by the synchronising calls.
  * n <= 1 returns 0 without device work. */
 int ips4o_sort(void *ptr, uint64_t n, int dtype, void *stream);
 
-/* As ips4o_sort with options (NULL = defaults) and optional statistics. */
+/* As ips4o_sort with options (NULL = defaults) and optional statistics
+ * (non-NULL `out` synchronises `stream` and reads the device's control block
+ * back; such a call is not capturable). */
 int ips4o_sort_ex(void *ptr, uint64_t n, int dtype, void *stream,
                   const ips4o_options *opt, ips4o_stats *out);
 
@@ -138,9 +156,21 @@ int ips4o_sort_ex(void *ptr, uint64_t n, int dtype, void *stream,
 int ips4o_sort_host(void *host_ptr, uint64_t n, int dtype,
                     const ips4o_options *opt, ips4o_stats *out);
 
-/* Upper bound of the device scratch bytes ips4o_sort_ex may allocate for
- * (n, dtype, opt) -- O(G*k*b*D + #tasks), "the scratch bytes are reported". */
+/* The device scratch bytes ips4o_sort_ex allocates for (n, dtype, opt)
+ * ("the scratch bytes are reported"): a control block, two task lists of
+ * n/(M+1)+2 records, and the level arena sized for the first two levels
+ * (O(G*k*b*D) per level plus 3 bytes per block; larger levels run in
+ * several rounds instead of growing it). */
 uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt);
+
+/* Error flags device code raised on `device` since the last clear (bit 0
+ * cleanup invariant, 1 task-list overflow, 2 a task without progress, 3 a
+ * device-side launch failure, 4 arena too small for one task).  Read it after
+ * synchronising the streams that ran sorts.  clear != 0 resets it. */
+int ips4o_device_status(int device, uint32_t *flags, int clear);
+
+/* Return the library's pooled scratch memory on `device` to the driver. */
+int ips4o_release_memory(int device);
 
 /* Human-readable text of a status code (for IPS4O_ERR_CUDA: the last CUDA
  * error string seen by this thread). */

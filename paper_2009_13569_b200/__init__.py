@@ -14,14 +14,14 @@ import os
 __all__ = [
     "U64", "F64", "PAIR", "REC100", "U32", "QUARTET", "TREE", "DIGIT",
     "load", "sort", "sort_ex", "sort_host", "partition_step", "classify",
-    "scratch_bytes", "dtype_info", "Options", "Stats", "IPS4OError",
+    "scratch_bytes", "dtype_info", "device_status", "release_memory", "Options", "Stats", "IPS4OError",
 ]
 
 U64, F64, PAIR, REC100, U32, QUARTET = 0, 1, 2, 3, 4, 5
 TREE, DIGIT = 0, 1
 ELEM_BYTES = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}
 KERNEL_NAMES = ["prepass", "sample", "classify", "boundaries", "stripe_fix", "permute",
-                "cleanup", "schedule", "basecase", "reverse", "host_plan", "total"]
+                "cleanup", "schedule", "basecase", "reverse", "plan", "total"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libips4o.so")
@@ -82,7 +82,8 @@ class StepInfo(ctypes.Structure):
 
 
 EXPORTS = ["ips4o_sort", "ips4o_sort_ex", "ips4o_sort_host", "ips4o_scratch_bytes",
-           "ips4o_status_string", "ips4o_get_dtype_info", "ips4o_partition_step", "ips4o_classify"]
+           "ips4o_status_string", "ips4o_get_dtype_info", "ips4o_partition_step", "ips4o_classify",
+           "ips4o_device_status", "ips4o_release_memory"]
 
 _lib = None
 
@@ -112,6 +113,10 @@ def load(path: str = LIB_PATH):
     L.ips4o_partition_step.restype = ci
     L.ips4o_classify.argtypes = [vp, u64, ci, vp, ci, ci, vp, vp]
     L.ips4o_classify.restype = ci
+    L.ips4o_device_status.argtypes = [ci, ctypes.POINTER(ctypes.c_uint32), ci]
+    L.ips4o_device_status.restype = ci
+    L.ips4o_release_memory.argtypes = [ci]
+    L.ips4o_release_memory.restype = ci
     _lib = L
     return L
 
@@ -184,6 +189,18 @@ def sort_host(a, dtype: int, **opts) -> dict:
     s = Stats()
     _check(load().ips4o_sort_host(ptr, nbytes // D, dtype, ctypes.byref(o), ctypes.byref(s)))
     return s.as_dict()
+
+
+def device_status(device: int = 0, clear: bool = False) -> int:
+    """Error flags the device code raised on ``device`` (0 = none); read after
+    synchronising the streams that ran sorts."""
+    f = ctypes.c_uint32(0)
+    _check(load().ips4o_device_status(device, ctypes.byref(f), int(clear)))
+    return int(f.value)
+
+
+def release_memory(device: int = 0) -> None:
+    _check(load().ips4o_release_memory(device))
 
 
 def scratch_bytes(n: int, dtype: int, **opts) -> int:

@@ -19,14 +19,22 @@ SRC = os.path.join(HERE, "csrc", "ips4o.cu")
 OUT = os.path.join(HERE, "lib", "libips4o.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+# Compile to LTO IR (relocatable device code: the recursion launches kernels
+# from the device, k_plan.cuh), then device-link with link-time optimisation
+# to sm_100a SASS: whole-program optimisation of the kernels comes back at
+# link time (measured: -rdc without LTO costs ~0.5 ms at 2^30, with LTO none).
+COMPILE_FLAGS = [
+    "-gencode", "arch=compute_100a,code=lto_100a", "-rdc=true",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-O3",
-    "-shared", "-cudart", "static",
     "--expt-relaxed-constexpr",
+]
+LINK_FLAGS = [
+    "-dlto", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
+FLAGS = COMPILE_FLAGS + LINK_FLAGS  # (reported by tools; build() runs the two steps)
 
 
 def sources():
@@ -57,18 +65,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     extra = extra_flags()
-    cmd = [NVCC, *FLAGS, *extra, "-o", OUT, SRC, "-lrt", "-ldl", "-lpthread"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    obj = OUT[:-3] + ".o"
+    cmds = [[NVCC, *COMPILE_FLAGS, *extra, "-c", "-o", obj, SRC],
+            [NVCC, *LINK_FLAGS, "-o", OUT, obj, "-lcudadevrt", "-lrt", "-ldl", "-lpthread"]]
     log = os.path.join(HERE, "lib", "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr[-8000:])
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        for cmd in cmds:
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            if res.returncode != 0:
+                sys.stderr.write(res.stderr[-8000:])
+                raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+    try:
+        os.remove(obj)
+    except OSError:
+        pass
     with open(STAMP, "w") as f:
         f.write(" ".join(extra) + "\n")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(open(log).read())
     return OUT
 
 

@@ -315,6 +315,27 @@ __device__ __forceinline__ int tile_load_async(char *s, const char *g, u64 nbyte
   return head;
 }
 
+// ------------------------------------------------------------------ device timing
+// Kernel durations without host events (the levels are launched from the
+// device): the first thread of every CTA lowers the slot's start, lane 0 of
+// every warp raises its end when it leaves the kernel (any return path).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+template <int SLOT> struct KTimer {
+  // holds a reference to the kernel parameter (no register kept live)
+  unsigned long long *const &ts;
+  __device__ __forceinline__ explicit KTimer(unsigned long long *const &tslots) : ts(tslots) {
+    if (ts && threadIdx.x == 0) atomicMin(&ts[2 * SLOT], gtimer());
+  }
+  __device__ __forceinline__ ~KTimer() {
+    if (ts && (threadIdx.x & 31) == 0) atomicMax(&ts[2 * SLOT + 1], gtimer());
+  }
+};
+#define KTIMER(tslots, slot) KTimer<slot> ktimer_(tslots)
+
 // ------------------------------------------------------------------ block scan
 // Exclusive scan of one u32 per thread over the first `n` threads of a CTA of
 // NT threads (n <= NT).  `ws` must hold NT/32 + 1 u32.  Returns the exclusive

@@ -94,13 +94,23 @@ struct LevelArgs {
                               // K3 moves with the block, K4 reads)
   u32 *task_done;             // [ntasks] no block of the task can be fetched any more (K4)
   // scheduler outputs
-  TaskDesc *next_tasks;       // next level
+  TaskDesc *next_tasks;       // pending list of the next round (tasks of the next level)
+  u32 *next_count;            // its length (atomic append; the planner preset it to the
+                              // number of tasks it deferred, DESIGN "Device planner")
   TaskDesc *base_tasks;       // base-case tasks of this level
   TaskDesc *split_tasks;      // base-case tasks of M < size <= 2M (split in two passes)
-  u32 *counters;              // [0] next count, [1] base count, [2] equal elems lo, [3] hi,
-                              // [4] cleanup invariant violations, [6..7] base elems, [8] split count
+  u32 *counters;              // [1] base count, [8] split count (per round); [2..3] equal
+                              // elems, [6..7] base elems (whole sort)
+  u32 *err;                   // error flags of the sort (ERR_*), never cleared
+  unsigned long long *tslot;  // device timing slots of this round [KS_COUNT][2] or null
   u32 next_cap;
   u32 base_cap_tasks;
+  u32 capture;                // test hook ips4o_partition_step: no scheduling
+  u32 bc_grid;                // base-case CTAs
+  void *ctl;                  // the sort's control block (SortCtl, k_plan.cuh)
+  const u32 *go;              // round 0 (host-launched): run only if *go != 0 (not an easy input)
+  u32 stages;                 // bit s set: stage s of this round runs (enum Stage)
+  u32 nmparts, nmtasks;       // K0m parts and tasks of this round (IPS2Ra)
   u64 base_cap_elems;         // base-case capacity M (elements)
   u64 base_split_elems;       // buckets up to this size go to the base case (2M when it can split)
   char *bc_scratch;           // K7 split scratch: [grid][M] items
@@ -122,6 +132,29 @@ constexpr u64 RBIAS = 1ull << 31;
 #define IPS4O_WR_STRIDE 4  // one 32-byte sector per bucket (8: 6.50 ms, 4: 6.37 ms, 16: 6.90 ms permute at 2^30)
 #endif
 constexpr int WR_STRIDE = IPS4O_WR_STRIDE;  // u64 words per bucket slot: [0] = packed (w, r), [1] = prefix end
+
+// Error flags a sort can raise on the device (SortCtl::error, and the
+// per-device status word behind ips4o_device_status).
+enum : u32 {
+  ERR_CLEANUP = 1,        // cleanup invariant: holes != overlap + partial buffers
+  ERR_LIST_OVERFLOW = 2,  // a task list was full (cannot happen with the planner's bounds)
+  ERR_NO_PROGRESS = 4,    // a child task equal to its parent (dropped, never looped on)
+  ERR_LAUNCH = 8,         // a device-side kernel launch failed
+  ERR_ARENA = 16,         // a single task does not fit the level arena
+};
+
+// Device timing slots (globaltimer, ns) per round: [slot][0] = earliest CTA
+// start, [slot][1] = latest warp end.  Host folds them into kernel families.
+enum KSlot {
+  KS_PRESAMPLE = 0, KS_PREPASS, KS_PREREDUCE, KS_MEASURE, KS_MEASURE_RED, KS_SAMPLE, KS_CLASSIFY,
+  KS_BOUND, KS_FIX, KS_PERM, KS_CSAVE, KS_CFILL, KS_BASE, KS_SPLIT, KS_REV, KS_PLAN, KS_COUNT
+};
+
+// The kernels of one round, in launch order (k_plan.cuh launch_stage).
+enum Stage {
+  ST_MEAS = 0, ST_MEASRED, ST_SAMPLE, ST_CLASSIFY, ST_BOUND, ST_FIX, ST_PERM, ST_CSAVE, ST_CFILL, ST_BASE,
+  ST_SPLIT, ST_NEXT, ST_N
+};
 
 struct PrepassOut {
   u32 nondecreasing;  // all adjacent pairs a[i] <= a[i+1]

@@ -269,6 +269,7 @@ struct BaseSplitArgs {
   u32 *next_count;      // its counter (K6 appended first)
   u32 next_cap;
   unsigned long long *base_elems;  // base-case element statistic (K6 counted the bucket)
+  u32 *err;             // error flags (ERR_LIST_OVERFLOW)
 };
 
 #ifdef IPS4O_PHASE_TIMING
@@ -284,7 +285,8 @@ struct BaseSplitArgs {
 
 template <int DT, bool SPLITK>
 __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
-    basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap, BaseSplitArgs sp) {
+    basecase_kernel(char *base, const TaskDesc *tasks, const u32 *count_ptr, u32 count_cap, BaseSplitArgs sp,
+                    unsigned long long *tslot) {
   using Tr = Traits<DT>;
   using BI = BaseItem<DT>;
   using Item = typename BI::Item;
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   u32 *s_big = reinterpret_cast<u32 *>(smem + S::off_big);
   u32 *s_ws = s_big + BIGCAP;  // scan workspace (NT/32+1)
   __shared__ u32 s_nbig, s_bigsum, s_dsplit, s_scnt;
+  KTIMER(tslot, SPLITK ? KS_SPLIT : KS_BASE);
   Item *scratch = reinterpret_cast<Item *>(sp.scratch) + (size_t)blockIdx.x * sp.cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   u32 count = *count_ptr;
@@ -572,6 +575,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         if (tid == 0) {
           const u32 slot = atomicAdd(sp.next_count, 1u);
           if (slot < sp.next_cap) sp.next_tasks[slot] = t;
+          else atomicOr(sp.err, (u32)ERR_LIST_OVERFLOW);
           atomicAdd(sp.base_elems, (unsigned long long)(-(long long)m));
         }
         __syncthreads();

@@ -46,6 +46,15 @@ __device__ __forceinline__ void tree_bucket_batch(const Key *tree, const Key *sp
   }
 }
 
+// The read-done bytes of the permutation (K4) for this stripe's block
+// positions start at 0; each stripe clears its own (no separate memset).
+template <int B>
+__device__ __forceinline__ void clear_read_flags(const LevelArgs &A, const LevelTask &L, u64 s0, u64 s1) {
+  unsigned char *f = A.rdone + L.blk_off;
+  const u64 b0 = s0 / B, b1 = (s1 + B - 1) / B;
+  for (u64 x = b0 + threadIdx.x; x < b1; x += blockDim.x) f[x] = 0;
+}
+
 template <int DT>
 struct ClsSmem {
   using Tr = Traits<DT>;
@@ -90,6 +99,8 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
   unsigned short *s_idx = reinterpret_cast<unsigned short *>(smem + S::off_idx);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_CLASSIFY);
   const u32 stripe = blockIdx.x;
   const u32 ti = A.stripe_task[stripe];
   const LevelTask &L = A.tasks[ti];
@@ -99,6 +110,7 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
   const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
   const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
   char *gtask = A.base + L.t.begin * (u64)D;
+  clear_read_flags<B>(A, L, s0, s1);
 
   if (ALGO == ALGO_TREE) {
     const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
@@ -342,6 +354,8 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   unsigned short *s_lut = reinterpret_cast<unsigned short *>(smem + S::off_lut);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_CLASSIFY);
   const u32 stripe = blockIdx.x;
   const u32 ti = A.stripe_task[stripe];
   const LevelTask &L = A.tasks[ti];
@@ -351,6 +365,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   const u64 s0 = (u64)(stripe - L.stripe_first) * L.stripe_elems;
   const u64 s1 = (s0 + L.stripe_elems < size) ? s0 + L.stripe_elems : size;
   Unit *gtask = reinterpret_cast<Unit *>(A.base + L.t.begin * (u64)Tr::D);
+  clear_read_flags<B>(A, L, s0, s1);
 
   if (ALGO == ALGO_TREE) {
     const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;

@@ -15,15 +15,23 @@ namespace ips4o {
 // final place [p*b, E_{j+1}).  Phase b then only writes holes.
 constexpr int CLN_WARPS = 8;
 
+// Grid: one CTA per (task, group of CLN_WARPS buckets), flattened into x
+// (gridDim.y would cap the tasks of a level at 65535).
+template <int DT> __host__ __device__ constexpr u32 cleanup_groups() {
+  return (u32)((Traits<DT>::KIDX + CLN_WARPS - 1) / CLN_WARPS);
+}
+
 template <int DT>
 __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
   using Unit = typename Tr::Unit;
   constexpr int D = Tr::D, B = Tr::B;
   constexpr int UPE = D / (int)sizeof(Unit);
-  const u32 ti = blockIdx.y;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_CSAVE);
+  const u32 ti = blockIdx.x / cleanup_groups<DT>();
   const LevelTask &L = A.tasks[ti];
-  const int j = blockIdx.x * CLN_WARPS + (threadIdx.x >> 5);
+  const int j = (int)(blockIdx.x % cleanup_groups<DT>()) * CLN_WARPS + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= (int)L.K) return;
   const u64 bo = L.bucket_off;
@@ -55,7 +63,7 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
     const u64 tl = W > hd ? W : hd;
     const u64 nholes = (hd - A.E[bo + j]) + (tl < E1 ? E1 - tl : 0);
     const u64 o = W > o0 ? W - o0 : 0;
-    if (nholes != o + A.ptot[bo + j]) atomicAdd(&A.counters[4], 1u);
+    if (nholes != o + A.ptot[bo + j]) atomicOr(A.err, (u32)ERR_CLEANUP);
   }
   if (ovb == (u32)j) {
     const u64 p0 = pblk * B;
@@ -76,7 +84,7 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
 // overlap element h for h < o, then the partial buffers in stripe order:
 // stripe s's buffer fills holes [o + pcum_s, o + pcum_s + pfill_s).  One CTA
 // per (stripe, task), a warp per bucket, coalesced copies of each buffer;
-// the CTA of stripe 0 also places the overlaps.
+// the CTA of stripe 0 also places the overlaps.  Grid: the level's stripes.
 constexpr int FILL_THREADS = 256;
 
 template <int DT>
@@ -86,10 +94,11 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
   constexpr int D = Tr::D, B = Tr::B;
   constexpr int UPE = D / (int)sizeof(Unit);
   constexpr int NW = FILL_THREADS / 32;
-  const u32 ti = blockIdx.y;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_CFILL);
+  const u32 ti = A.stripe_task[blockIdx.x];
   const LevelTask &L = A.tasks[ti];
-  const u32 s = blockIdx.x;
-  if (s >= L.nstripes) return;
+  const u32 s = blockIdx.x - L.stripe_first;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u64 bo = L.bucket_off;
   char *gtask = A.base + L.t.begin * (u64)D;
@@ -127,16 +136,15 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
 // Equality buckets (odd index 2i+1, i < s) are terminal; buckets
 // of at most one element are done; buckets of at most M elements (the
 // one-CTA base-case capacity, the GPU analogue of "at most 2 n_0")
-// go to the base-case list; the rest form the next level.  Child key bounds
-// come from the splitters (TREE) or the digit (DIGIT).
-constexpr int SCHED_THREADS = 256;
-
+// go to the base-case list; the rest are appended to the pending list of the
+// next round.  Child key bounds come from the splitters (TREE) or the digit
+// (DIGIT).  Runs inside the boundaries kernel (K3a), by all threads of the
+// task's CTA, once E is known: nothing it reads changes after K3a.
 template <int DT, int ALGO>
-__global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
+__device__ void schedule_task(const LevelArgs &A, u32 ti, const u64 *sE) {
   using Tr = Traits<DT>;
   using Key = typename Tr::Key;
   constexpr int KI = Tr::KIDX;
-  const u32 ti = blockIdx.x;
   const LevelTask &L = A.tasks[ti];
   const int K = (int)L.K;
   Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
@@ -148,8 +156,8 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
   }
   const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
   const Key *spl = gt + KI;
-  for (int j = threadIdx.x; j < K; j += SCHED_THREADS) {
-    const u64 e0 = A.E[L.bucket_off + j], e1 = A.E[L.bucket_off + j + 1];
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const u64 e0 = sE[j], e1 = sE[j + 1];
     const u64 sz = e1 - e0;
     if (sz == 0) continue;
     Key lo = plo, hi = phi;
@@ -188,6 +196,12 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
       if (sz > 1) atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[2]), (unsigned long long)sz);
       continue;
     }
+    if (sz == L.t.size && lo == plo && hi == phi && ALGO == ALGO_TREE) {
+      // a child identical to its parent would be partitioned again forever
+      // (cannot happen with >= 3 splitters, k_max >= 4); report, never loop
+      atomicOr(A.err, (u32)ERR_NO_PROGRESS);
+      continue;
+    }
     TaskDesc c;
     c.begin = L.t.begin + e0;
     c.size = sz;
@@ -198,21 +212,24 @@ __global__ void __launch_bounds__(SCHED_THREADS) schedule_kernel(LevelArgs A) {
     // DIGIT: a digit that kept most of the task splits bits the keys do not
     // use (sparse keys); measure the child's exact range first (DESIGN R27)
     if (ALGO == ALGO_DIGIT && 2 * sz > L.t.size) c.flags = TF_MEASURE;
+    u32 *cnt;
+    TaskDesc *list;
+    u32 cap;
     if (sz <= A.base_cap_elems) {
-      u32 slot = atomicAdd(&A.counters[1], 1u);
-      if (slot < A.base_cap_tasks) A.base_tasks[slot] = c;
+      cnt = &A.counters[1], list = A.base_tasks, cap = A.base_cap_tasks;
       atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
     } else if (sz <= A.base_split_elems ||
                (BaseItem<DT>::KEY_ONLY && sz <= 65535 && hi - lo < (Key)basecase_count_range<DT>())) {
       // up to twice the capacity: the base case's two-pass split (K7s); a
       // narrow key range of a key-only type: counted exactly (any size)
-      u32 slot = atomicAdd(&A.counters[8], 1u);
-      if (slot < A.base_cap_tasks) A.split_tasks[slot] = c;
+      cnt = &A.counters[8], list = A.split_tasks, cap = A.base_cap_tasks;
       atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
     } else {
-      u32 slot = atomicAdd(&A.counters[0], 1u);
-      if (slot < A.next_cap) A.next_tasks[slot] = c;
+      cnt = A.next_count, list = A.next_tasks, cap = A.next_cap;
     }
+    const u32 slot = atomicAdd(cnt, 1u);
+    if (slot < cap) list[slot] = c;
+    else atomicOr(A.err, (u32)ERR_LIST_OVERFLOW);
   }
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "k_classify.cuh"
+#include "k_cleanup.cuh"
 
 namespace ips4o {
 
@@ -11,12 +12,15 @@ namespace ips4o {
 // the exact boundaries E (prefix sum), the block-rounded delimiters
 // d_j = ceil(E_j / b) * b, the full blocks per bucket, and initialises
 // the packed (w, r) words: w_j = d_j / b, r_j = w_j + f_j - 1.
+// Then the same CTA schedules the task's buckets (K6, schedule_task).
 constexpr int BND_THREADS = 1024;
 
-template <int DT>
+template <int DT, int ALGO>
 __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
   constexpr int KI = Tr::KIDX, B = Tr::B;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_BOUND);
   constexpr int QB = BND_THREADS / KI;  // threads per bucket, each over a share of the stripes
   static_assert(KI * QB == BND_THREADS, "whole threads per bucket");
   __shared__ u32 ws[BND_THREADS / 32 + 1];
@@ -96,6 +100,10 @@ __global__ void __launch_bounds__(BND_THREADS) boundaries_kernel(LevelArgs A) {
     A.E[bo + K] = L.t.size;
     A.ovf_used[ti] = 0xFFFFFFFFu;
   }
+  if (!A.capture) {
+    __syncthreads();
+    schedule_task<DT, ALGO>(A, ti, s_E);
+  }
 }
 
 // ------------------------------------------------------------------ K3b
@@ -111,6 +119,8 @@ constexpr int FIX_THREADS = 256;
 template <int DT>
 __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_FIX);
   using Unit = typename Tr::Unit;
   constexpr int D = Tr::D, B = Tr::B;
   constexpr int NU = B * D / (int)sizeof(Unit);
@@ -311,6 +321,8 @@ __global__ void __launch_bounds__(PERM_THREADS, IPS4O_PERM_MINB) permute_kernel(
   constexpr int NU = B * D / (int)sizeof(Unit);
   constexpr int NPL = (NU + 31) / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_PERM);
   const u32 home = A.perm_task[blockIdx.x];
   if (A.dbg_one_agent && wid != 0) return;
   const u32 agent = (blockIdx.x - A.tasks[home].perm_first) * PERM_WARPS + wid;

@@ -134,6 +134,8 @@ template <int DT, int ALGO>
 __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   using Tr = Traits<DT>;
   using Key = typename Tr::Key;
+  if (A.go && *A.go == 0) return;  // round 0 of an easy input (k_plan.cuh)
+  KTIMER(A.tslot, KS_SAMPLE);
   const int ti = blockIdx.x;
   LevelTask &L = A.tasks[ti];
   if (ALGO == ALGO_DIGIT) {

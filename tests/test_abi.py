@@ -49,6 +49,15 @@ def test_built_for_sm100a():
     assert "sm_100a" in out
 
 
+def _has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
 def test_argument_validation_without_gpu(lib):
     import paper_2009_13569_b200 as p
 
@@ -58,8 +67,26 @@ def test_argument_validation_without_gpu(lib):
     # unknown dtype, NULL pointer, misaligned pointer
     assert lib.ips4o_sort(None, 10, 7, None) == -1
     assert lib.ips4o_sort(None, 10, p.U64, None) == -1
-    assert lib.ips4o_sort(ctypes.c_void_p(8), 10, p.U64, None) == -1
+    # alignment: 4 B for U32, 8 B for U64/F64, 16 B for the others (ips4o.h)
+    assert lib.ips4o_sort(ctypes.c_void_p(4), 10, p.U64, None) == -1
+    assert lib.ips4o_sort(ctypes.c_void_p(2), 10, p.U32, None) == -1
+    assert lib.ips4o_sort(ctypes.c_void_p(8), 10, p.PAIR, None) == -1
+    assert lib.ips4o_sort(ctypes.c_void_p(8), 10, p.REC100, None) == -1
     assert lib.ips4o_sort(ctypes.c_void_p(16), 1 << 32, p.U64, None) == -1
+    # k_max < 4 is rejected for the tree (no progress guarantee), allowed for digits
+    o = p.Options()
+    o.k_max = 2
+    assert lib.ips4o_sort_ex(ctypes.c_void_p(16), 10, p.U64, None, ctypes.byref(o), None) == -1
+    o.k_max = 3
+    o.algo = p.DIGIT
+    assert lib.ips4o_sort_ex(ctypes.c_void_p(16), 10, p.U64, None, ctypes.byref(o), None) == -1
+    # well-formed calls on a machine without a GPU report it
+    if not _has_gpu():
+        assert lib.ips4o_sort(ctypes.c_void_p(8), 10, p.U64, None) == -4
+        o.k_max = 2
+        assert lib.ips4o_sort_ex(ctypes.c_void_p(16), 10, p.U64, None, ctypes.byref(o), None) == -4
+        f = ctypes.c_uint32(7)
+        assert lib.ips4o_device_status(0, ctypes.byref(f), 0) == 0 and f.value == 0
     assert lib.ips4o_status_string(-1).decode() == "invalid argument"
     assert "sm_100" in lib.ips4o_status_string(-4).decode()
 
