@@ -227,6 +227,9 @@ template <int DT> static SortCfg make_cfg(const Call &k, const DevState &ds, cha
   c.timing = k.timing;
   c.capture = k.capture;
   c.dbg_one_agent = env_int("IPS4O_DEBUG_ONE_AGENT", 0, 0, 1);
+  // profiling mode: every round launched from the host (one synchronisation
+  // per round) so that ncu sees each kernel; same plans, grids and kernels
+  c.host_levels = k.capture ? 0 : env_int("IPS4O_HOST_LEVELS", 0, 0, 1);
   c.sms = ds.sms;
   // stripes per SM: smaller CTAs shorten the tail of levels of unequal tasks
   c.spm = env_int("IPS4O_STRIPES_PER_SM", 6, 1, 8);
@@ -355,7 +358,14 @@ template <int DT> struct Sorter {
     c.arena_cap = sp.arena_cap;
     c.status = ds->status;
     if (scratch_out) *scratch_out = sp.total;
-    const u64 host_launches = k.algo == ALGO_TREE ? enqueue<ALGO_TREE>(c, st) : enqueue<ALGO_DIGIT>(c, st);
+    u64 host_launches = k.algo == ALGO_TREE ? enqueue<ALGO_TREE>(c, st) : enqueue<ALGO_DIGIT>(c, st);
+    if (c.host_levels && !(c.n <= c.base_cap)) {
+      rc = k.algo == ALGO_TREE ? host_rounds<ALGO_TREE>(c, st, host_launches) : host_rounds<ALGO_DIGIT>(c, st, host_launches);
+      if (rc) {
+        cudaFreeAsync(scratch, st);
+        return rc;
+      }
+    }
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) {
       cudaFreeAsync(scratch, st);
@@ -422,6 +432,29 @@ template <int DT> struct Sorter {
     return nl;
   }
 
+  // Profiling mode: the device planner plans each later round (phase 3, no
+  // launches); the host reads the plan back and launches the round.
+  template <int ALGO> static int host_rounds(const SortCfg &c, cudaStream_t st, u64 &nl) {
+    SortCtl *ctl = reinterpret_cast<SortCtl *>(c.scratch);
+    for (;;) {
+      u32 r0 = 0, r1 = 0;
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(&r0, &ctl->round, 4, cudaMemcpyDeviceToHost));
+      driver_kernel<DT, ALGO><<<1, PLAN_THREADS, 0, st>>>(ctl, 3);
+      ++nl;
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(&r1, &ctl->round, 4, cudaMemcpyDeviceToHost));
+      if (r1 == r0) return 0;  // nothing planned: the sort is done
+      LevelArgs A;
+      CK(cudaMemcpy(&A, &ctl->A, sizeof A, cudaMemcpyDeviceToHost));
+      for (int s = 0; s < ST_N; ++s)
+        if ((A.stages >> s) & 1u) {
+          host_stage<ALGO>(A, s, st);
+          ++nl;
+        }
+    }
+  }
+
   template <int ALGO> static void host_stage(const LevelArgs &A, int s, cudaStream_t st) {
     using Tr = Traits<DT>;
     SortCtl *ctl = reinterpret_cast<SortCtl *>(A.ctl);
@@ -452,7 +485,9 @@ template <int DT> struct Sorter {
         break;
       }
       case ST_NEXT: driver_kernel<DT, ALGO><<<1, PLAN_THREADS, 0, st>>>(ctl, 2); break;
-      default: break;  // (no K0m at round 0: the root is never TF_MEASURE)
+      case ST_MEAS: measure_part_kernel<DT><<<A.nmparts, MEAS_THREADS, 0, st>>>(A); break;
+      case ST_MEASRED: measure_reduce_kernel<DT><<<(A.nmtasks + 127) / 128, 128, 0, st>>>(A, A.nmtasks); break;
+      default: break;
     }
   }
 

@@ -45,6 +45,7 @@ struct SortCfg {
   u64 base_split;      // buckets up to this size go to the base case (2M when it can split)
   int algo, k_max, alpha_min, max_levels;
   int skip_prepass, skip_basecase, timing, capture, dbg_one_agent;
+  int host_levels;     // profiling mode (IPS4O_HOST_LEVELS=1): the host launches every round
   int sms;             // SMs of the device
   int spm;             // classification stripes per SM
   u32 g_perm;          // permutation CTAs per level (SMs x occupancy)
@@ -245,7 +246,7 @@ __host__ __device__ LevelArgs level_args(SortCtl *ctl, const SortCfg &c, const P
     stg |= 1u << ST_BASE;
     if (BaseItem<DT>::SPLIT) stg |= 1u << ST_SPLIT;
   }
-  if (!c.capture) stg |= 1u << ST_NEXT;
+  if (!c.capture && !c.host_levels) stg |= 1u << ST_NEXT;
   A.stages = stg;
   return A;
 }
@@ -611,8 +612,8 @@ __global__ void __launch_bounds__(PLAN_THREADS) driver_kernel(SortCtl *ctl, int 
   const u32 r = ctl->round;
   unsigned long long *const kts = c.timing ? &ctl->tslot[phase == 1 ? 0 : (r < MAX_ROUNDS ? r : MAX_ROUNDS - 1)][0][0] : nullptr;
   KTIMER(kts, KS_PLAN);
-  if (phase == 2) {
-    plan_round<DT, ALGO>(ctl, true);
+  if (phase >= 2) {  // 3: plan only (profiling mode: the host launches the round)
+    plan_round<DT, ALGO>(ctl, phase == 2);
     return;
   }
   if (!ctl->need_prepass) return;  // (host-launched after the pre-pass kernels)

@@ -113,8 +113,9 @@ def test_pointer_alignment_per_dtype(ips, orc):
 
 
 def test_level_with_more_than_65535_tasks(ips, orc):
-    """A small base-case capacity forces > 65535 tasks in one level (the
-    cleanup grids are flattened; gridDim.y would cap them at 65535)."""
+    """A small base-case capacity forces > 65535 tasks at level 3 (the cleanup
+    grids are flattened; gridDim.y would cap them at 65535).  The arena, sized
+    for the first two levels, runs that level in several rounds."""
     import torch
 
     n = 1 << 25
@@ -122,7 +123,7 @@ def test_level_with_more_than_65535_tasks(ips, orc):
     t = to_dev(a)
     st = ips.sort_ex(t, U64, base_cap=64)
     g = from_dev(t, a)
-    assert max(st["tasks_per_level"]) > 65535, st["tasks_per_level"]
+    assert sum(st["tasks_per_level"][2:]) > 65535, st["tasks_per_level"]
     assert orc.parity(g, orc.sort(a, U64), U64) == -1
     del t
     torch.cuda.empty_cache()
