@@ -91,7 +91,10 @@ typedef struct ips4o_options {
                               unsorted)                                               */
     int32_t timing;        /* 1 = record per-kernel device times into ips4o_stats
                               (device globaltimer stamps per kernel; needs `out`)    */
-    int32_t reserved[7];
+    int32_t arena_mb;      /* level arena in MiB (0 = sized for the first two levels;
+                              at least the root level's plan); a level that does not
+                              fit runs in several rounds                            */
+    int32_t reserved[6];
 } ips4o_options;
 
 #define IPS4O_MAX_LEVELS_REPORTED 16

@@ -37,7 +37,7 @@ class Options(ctypes.Structure):
         ("algo", ctypes.c_int32), ("k_max", ctypes.c_int32), ("seed", ctypes.c_uint64),
         ("alpha_min", ctypes.c_int32), ("base_cap", ctypes.c_int32), ("max_levels", ctypes.c_int32),
         ("skip_prepass", ctypes.c_int32), ("skip_basecase", ctypes.c_int32), ("timing", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("arena_mb", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6),
     ]
 
 
@@ -128,8 +128,9 @@ def _check(rc: int):
 
 
 def _options(algo=TREE, k_max=0, seed=0, alpha_min=0, base_cap=0, max_levels=0,
-             skip_prepass=False, skip_basecase=False, timing=False) -> Options:
+             skip_prepass=False, skip_basecase=False, timing=False, arena_mb=0) -> Options:
     o = Options()
+    o.arena_mb = arena_mb
     o.algo, o.k_max, o.seed, o.alpha_min = algo, k_max, seed, alpha_min
     o.base_cap, o.max_levels = base_cap, max_levels
     o.skip_prepass, o.skip_basecase, o.timing = int(skip_prepass), int(skip_basecase), int(timing)

@@ -233,6 +233,16 @@ template <> __host__ __device__ __forceinline__ u64 key_max<u64>() { return ~0ul
 template <> __host__ __device__ __forceinline__ u128 key_max<u128>() { return (((u128)1) << 80) - 1; }
 template <> __host__ __device__ __forceinline__ K192 key_max<K192>() { return K192(~0ull, ~0ull, ~0ull); }
 
+// ------------------------------------------------------------------ lookup table of starting leaves
+// (P:4049-4050).  Slot q of a task's table covers [llo + q*2^ls, llo +
+// (q+1)*2^ls) (slot 0 also every key below, the last slot every key above).
+// A 16-bit entry holds either the final bucket (LUT_FIN, no splitter in the
+// slot) or a = #{splitters < the slot's first key} (9 bits) and the number c
+// of splitters inside it (6 bits, 63 = "63 or more").
+constexpr int LUT_BITS = 14;
+constexpr u32 LUT_SLOTS = 1u << LUT_BITS;
+constexpr u32 LUT_FIN = 1u << 15;
+
 // ------------------------------------------------------------------ RNG (DESIGN R8)
 constexpr u64 GAMMA = 0x9E3779B97F4A7C15ull;
 __host__ __device__ __forceinline__ u64 mix64(u64 z) {

@@ -60,8 +60,13 @@ struct LevelTask {
   int shift;         // digit shift (DIGIT)
   u32 k_used;        // k after the equality-budget rule (DESIGN R10)
   u32 pad1;
-  u64 lut_lo[KEY_WORDS];  // key range of the sample (TREE): the classifier's lookup
-  u64 lut_hi[KEY_WORDS];     // table spans [lut_lo, lut_hi] inside [t.lo, t.hi]
+  u64 lut_lo[KEY_WORDS];  // key range of the sample (TREE); after K1: the first key of
+  u64 lut_hi[KEY_WORDS];  // the lookup table's slot 1 grid (llo) and the sample maximum
+  u32 lut_ls;             // lookup table (K1 builds it once per task): slot of key x =
+  u32 lut_n;              //   min((x - llo) >> lut_ls, lut_n - 1) (x >= llo), else 0
+  u32 lut_span;           // the table spans the task's bounds (no clamping needed)
+  u32 lut_bits;           // the table has 2^lut_bits slots (planner: from the bucket count)
+  u64 lut_off;            // its offset (in slots) in the level's table array
 };
 
 // Device pointers of one level's scratch arrays (all in one arena).
@@ -75,6 +80,7 @@ struct LevelArgs {
   const u32 *stripe_task;     // [nstripes] -> task index
   const u32 *perm_task;       // [nperm] -> task index
   void *trees;                // [ntasks][2][KIDX] keys (tree | splitter)
+  unsigned short *luts;       // [lut_off + q] lookup tables of starting leaves (K1 -> K2)
   u32 *counts;                // [stripe-bucket slot] elements per bucket per stripe
   u32 *pfill;                 // [stripe-bucket slot] elements left in partial buffers
   u32 *pcum;                  // [stripe-bucket slot] exclusive prefix over the task's stripes of pfill

@@ -164,14 +164,14 @@ struct ScratchPlan {
   u64 ctl_bytes, list_cap, list_bytes, arena_off, arena_cap, total;
 };
 
-template <int DT> static ScratchPlan scratch_plan(const SortCfg &c) {
+template <int DT> static ScratchPlan scratch_plan(const SortCfg &c, u64 arena_bytes) {
   ScratchPlan s;
   s.ctl_bytes = rup(sizeof(SortCtl), 256);
   // a pending task is larger than M and tasks are disjoint (DESIGN "Device planner")
   s.list_cap = c.n / (c.base_cap + 1) + 2;
   s.list_bytes = rup(2 * s.list_cap * sizeof(TaskDesc), 256);
   s.arena_off = s.ctl_bytes + s.list_bytes;
-  s.arena_cap = host_arena_bytes<DT>(c);
+  s.arena_cap = host_arena_bytes<DT>(c, arena_bytes);
   s.total = s.arena_off + s.arena_cap;
   return s;
 }
@@ -183,6 +183,7 @@ struct Call {
   int alpha_min = 64;
   u64 base_cap = 0;
   int max_levels = 0;
+  u64 arena_bytes = 0;
   bool skip_prepass = false, skip_basecase = false, timing = false, capture = false;
 };
 
@@ -205,6 +206,8 @@ static int parse_options(Call &k, const ips4o_options *opt) {
   k.skip_prepass = opt->skip_prepass != 0;
   k.skip_basecase = opt->skip_basecase != 0;
   k.timing = opt->timing != 0;
+  if (opt->arena_mb < 0) return IPS4O_ERR_INVALID;
+  k.arena_bytes = (u64)opt->arena_mb << 20;
   return 0;
 }
 
@@ -238,14 +241,14 @@ template <int DT> static SortCfg make_cfg(const Call &k, const DevState &ds, cha
   return c;
 }
 
-static u64 scratch_for(int dtype, const SortCfg &c) {
+static u64 scratch_for(int dtype, const SortCfg &c, u64 arena_bytes) {
   switch (dtype) {
-    case DT_U64: return scratch_plan<DT_U64>(c).total;
-    case DT_F64: return scratch_plan<DT_F64>(c).total;
-    case DT_PAIR: return scratch_plan<DT_PAIR>(c).total;
-    case DT_REC100: return scratch_plan<DT_REC100>(c).total;
-    case DT_U32: return scratch_plan<DT_U32>(c).total;
-    default: return scratch_plan<DT_QUARTET>(c).total;
+    case DT_U64: return scratch_plan<DT_U64>(c, arena_bytes).total;
+    case DT_F64: return scratch_plan<DT_F64>(c, arena_bytes).total;
+    case DT_PAIR: return scratch_plan<DT_PAIR>(c, arena_bytes).total;
+    case DT_REC100: return scratch_plan<DT_REC100>(c, arena_bytes).total;
+    case DT_U32: return scratch_plan<DT_U32>(c, arena_bytes).total;
+    default: return scratch_plan<DT_QUARTET>(c, arena_bytes).total;
   }
 }
 
@@ -345,7 +348,7 @@ template <int DT> struct Sorter {
     rc = k.algo == ALGO_TREE ? ensure_attrs<DT, ALGO_TREE>(ds) : ensure_attrs<DT, ALGO_DIGIT>(ds);
     if (rc) return rc;
     SortCfg c = make_cfg<DT>(k, *ds, base, n);
-    const ScratchPlan sp = scratch_plan<DT>(c);
+    const ScratchPlan sp = scratch_plan<DT>(c, k.arena_bytes);
     char *scratch = nullptr;
     if (cudaMallocFromPoolAsync((void **)&scratch, sp.total, ds->pool, st) != cudaSuccess) {
       cudaGetLastError();
@@ -703,7 +706,7 @@ uint64_t ips4o_scratch_bytes(uint64_t n, int dtype, const ips4o_options *opt) {
     case DT_U32: c = make_cfg<DT_U32>(k, tmp, nullptr, n); break;
     default: c = make_cfg<DT_QUARTET>(k, tmp, nullptr, n); break;
   }
-  return scratch_for(dtype, c);
+  return scratch_for(dtype, c, k.arena_bytes);
 }
 
 int ips4o_device_status(int device, uint32_t *flags, int clear) {

@@ -380,60 +380,24 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   }
   u32 myfill = 0;  // tid < KI: elements buffered for bucket tid
 
-  // Lookup table of starting leaves: slot q covers
-  // [llo + q*2^ls, llo + (q+1)*2^ls).  A 16-bit entry holds either the final
-  // bucket (FIN, no splitter in the slot) or a = #{splitters < its first key}
-  // (9 bits) and the number c of splitters inside it (6 bits, 63 = "63 or
-  // more"): c = 1, the common case, takes one comparison.
-  const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
-  Key llo = tlo, lhi = thi;
+  // Lookup table of starting leaves, built once per task by K1
+  // (build_lut): copied into shared memory, 32 B per thread.
+  const Key tlo = key_from_words<Key>(L.t.lo);
+  Key llo = tlo;
+  int ls = 0;
+  u32 nlut_used = 1;
+  bool span_task = false;
+  const int nspl = (1 << l) - 1;
+  constexpr u32 FIN = LUT_FIN;
+  static_assert(KI <= 512, "bucket and splitter indices fit 9 bits");
+  static_assert(S::LUT_BITS == LUT_BITS, "table size");
   if (ALGO == ALGO_TREE) {
     llo = key_from_words<Key>(L.lut_lo);
-    lhi = key_from_words<Key>(L.lut_hi);
-    if (llo < tlo) llo = tlo;
-    if (lhi > thi) lhi = thi;
-    if (lhi < llo) lhi = llo;
-  }
-  // When the sample's range covers a good part of the task's bounds, the
-  // table spans the bounds themselves: every key then maps to a slot without
-  // clamping (keys outside the sample range only in the first/last slots
-  // otherwise).
-  const bool span_task = ALGO == ALGO_TREE && (lhi - llo) >= ((thi - tlo) >> 2);
-  if (span_task) {
-    llo = tlo;
-    lhi = thi;
-  }
-  int ls = bitlen((Key)(lhi - llo)) - S::LUT_BITS;
-  if (ls < 0) ls = 0;
-  const u32 nlut_used = (u32)((lhi - llo) >> ls) + 1;
-  const int nspl = (1 << l) - 1;
-  constexpr u32 FIN = 1u << 15;  // table entry holds the final bucket
-  static_assert(KI <= 512, "bucket and splitter indices fit 9 bits");
-  if (ALGO == ALGO_TREE) {
-    __syncthreads();
-    auto lower = [&](Key v) -> u32 {  // #{splitter[i] < v, i < s}
-      u32 a = 0, b = (u32)nspl;
-      while (a < b) {
-        u32 mid = (a + b) >> 1;
-        if (s_spl[mid] < v) a = mid + 1;
-        else b = mid;
-      }
-      return a;
-    };
-    for (u32 q = tid; q < (1u << S::LUT_BITS); q += NT) {
-      u32 e = 0;
-      if (q < nlut_used) {
-        const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
-        const Key r1 = q + 1 == nlut_used ? thi : llo + (((Key)(q + 1)) << ls) - 1;
-        // a = #{splitters < r0}; the count covers splitters in [r0, r1] (a
-        // slot with none cannot hold a key equal to a splitter)
-        const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
-        // no splitter in the slot: no key in it equals one, so key < s_a,
-        // except above the last splitter (bucket 2s+1 with equality buckets)
-        e = b == a ? FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | (min(b - a, 63u) << 9);
-      }
-      s_lut[q] = (unsigned short)e;
-    }
+    ls = (int)L.lut_ls;
+    nlut_used = L.lut_n;
+    span_task = L.lut_span != 0;
+    const uint4 *src = reinterpret_cast<const uint4 *>(A.luts + L.lut_off);
+    for (u32 q = tid; q < (2u << L.lut_bits) / 16; q += NT) reinterpret_cast<uint4 *>(s_lut)[q] = src[q];
   }
   const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
   Key kmin = key_max<Key>(), kmax = (Key)0;

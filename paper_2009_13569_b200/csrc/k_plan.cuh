@@ -91,7 +91,7 @@ template <int DT> __host__ __device__ u64 level_stripe_elems(const SortCfg &c, u
 }
 
 struct TaskShape {
-  u32 kr, kidx, m, ns, np, mparts;
+  u32 kr, kidx, m, ns, np, mparts, lut_bits, lut_slots;
   u64 se_t, nblk;
 };
 
@@ -134,11 +134,17 @@ template <int DT> __host__ __device__ TaskShape task_shape(const SortCfg &c, u64
     mp = mp > MEAS_MAXPARTS ? MEAS_MAXPARTS : mp;
   }
   s.mparts = (u32)mp;
+  // lookup table of starting leaves (TREE, 4/8/16-byte keys): ~64 slots per
+  // bucket index, at most LUT_SLOTS
+  u32 lb = 6;
+  while ((1u << (lb - 6)) < s.kidx) ++lb;
+  s.lut_bits = lb < (u32)LUT_BITS ? lb : (u32)LUT_BITS;
+  s.lut_slots = (Tr::D <= 16 && c.algo == ALGO_TREE) ? (1u << s.lut_bits) : 0u;
   return s;
 }
 
 struct PlanTotals {
-  u64 T, S, NP, nbk, nsbk, nblk, child, mparts, mtasks;
+  u64 T, S, NP, nbk, nsbk, nblk, child, mparts, mtasks, luts;
   u64 max_m, bc_grid, bc_cap;
 };
 
@@ -152,6 +158,7 @@ __host__ __device__ __forceinline__ void add_shape(PlanTotals &P, const TaskShap
   P.child += s.kidx;
   P.mparts += s.mparts;
   P.mtasks += s.mparts ? 1 : 0;
+  P.luts += s.lut_slots;
   P.max_m = P.max_m > s.m ? P.max_m : s.m;
 }
 
@@ -170,6 +177,7 @@ template <int DT> __host__ __device__ u64 layout(LevelArgs &A, char *base, const
   A.stripe_task = reinterpret_cast<const u32 *>(take(P.S * 4));
   A.perm_task = reinterpret_cast<const u32 *>(take(P.NP * 4));
   A.trees = take(P.T * 2 * KI * sizeof(Key));
+  A.luts = reinterpret_cast<unsigned short *>(take(P.luts * 2));
   A.counts = reinterpret_cast<u32 *>(take(P.nsbk * 4));
   A.pfill = reinterpret_cast<u32 *>(take(P.nsbk * 4));
   A.pcum = reinterpret_cast<u32 *>(take(P.nsbk * 4));
@@ -260,13 +268,15 @@ template <int DT> __host__ __device__ PlanTotals root_totals(const SortCfg &c) {
 // Host: arena capacity = the larger of the root level's plan and the plan of
 // a second level of k' equal tasks (its more numerous stripes, trees and
 // overlap blocks); skewed levels beyond it are split into rounds.
-template <int DT> u64 host_arena_bytes(const SortCfg &c) {
+// (min_bytes > 0: the caller's arena size, at least the root level's plan)
+template <int DT> u64 host_arena_bytes(const SortCfg &c, u64 min_bytes = 0) {
   PlanTotals P1{};
   const u64 n = c.n;
   const u64 se1 = level_stripe_elems<DT>(c, n);
   const TaskShape r = task_shape<DT>(c, n, 0, se1, n);
   add_shape(P1, r);
   u64 b = plan_bytes<DT>(P1, c);
+  if (min_bytes) return rup(b > min_bytes ? b : min_bytes, 4096);
   const u64 k1 = r.kr, child = n / (k1 ? k1 : 1);
   if (child > c.base_split) {
     PlanTotals P2{};
@@ -326,6 +336,7 @@ __device__ PlanTotals round_totals(const SortCfg &c, const TaskDesc *P, u32 q, u
   T.child = block_sum_u64(L.child, ws);
   T.mparts = block_sum_u64(L.mparts, ws);
   T.mtasks = block_sum_u64(L.mtasks, ws);
+  T.luts = block_sum_u64(L.luts, ws);
   T.max_m = block_max_u64(L.max_m, ws);
   return T;
 }
@@ -461,7 +472,7 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
   // ---- per-task records: a contiguous chunk of tasks per thread, offsets by scans
   const u32 per = (q + PLAN_THREADS - 1) / PLAN_THREADS;
   const u32 i0 = tid * per < q ? tid * per : q, i1 = i0 + per < q ? i0 + per : q;
-  u32 ls = 0, lp = 0, lbk = 0, lsbk = 0, lmp = 0, lmt = 0;
+  u32 ls = 0, lp = 0, lbk = 0, lsbk = 0, lmp = 0, lmt = 0, llut = 0;
   u64 lblk = 0;
   for (u32 i = i0; i < i1; ++i) {
     const TaskShape s = task_shape<DT>(c, P[i].size, P[i].flags, se, N);
@@ -472,6 +483,7 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
     lblk += s.nblk;
     lmp += s.mparts;
     lmt += s.mparts ? 1 : 0;
+    llut += s.lut_slots;
   }
   u32 tt;
   u32 os = block_exclusive_scan<PLAN_THREADS>(ls, s_ws, &tt);
@@ -482,6 +494,7 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
   u32 omt = block_exclusive_scan<PLAN_THREADS>(lmt, s_ws, &tt);
   // nblk can exceed 2^32 / PLAN_THREADS per thread only for n >= 2^32 (rejected)
   u64 oblk = block_exclusive_scan<PLAN_THREADS>((u32)lblk, s_ws, &tt);
+  u64 olut = block_exclusive_scan<PLAN_THREADS>(llut, s_ws, &tt);
   u32 *stripe_task = const_cast<u32 *>(A.stripe_task);
   u32 *perm_task = const_cast<u32 *>(A.perm_task);
   u32 *mpart = const_cast<u32 *>(A.measure_part);
@@ -502,6 +515,8 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
     L.bucket_off = obk;
     L.blk_off = oblk;
     L.sbk_off = osbk;
+    L.lut_bits = s.lut_bits;
+    L.lut_off = olut;
     A.tasks[i] = L;
     if (s.mparts) {
       mtask[3 * omt] = i;
@@ -519,6 +534,7 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
     obk += s.kidx + 1;
     osbk += s.ns * s.kidx;
     oblk += s.nblk;
+    olut += s.lut_slots;
     A.task_done[i] = 0;
   }
   __syncthreads();

@@ -129,6 +129,62 @@ __device__ __forceinline__ void digit_setup(LevelTask &L) {
   L.k_used = 1u << bits;
 }
 
+// The lookup table of starting leaves of a task, built once
+// here for all classification CTAs of the task.  Padded splitters
+// spl[i] = cand[min(i, u-1)], i < s = 2^l - 1; the table spans
+// the sample's key range inside the task's bounds, or the bounds themselves
+// when the sample covers a good part of them (every key then falls into a
+// slot without clamping).
+template <class Key>
+__device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *cand, int u, int l) {
+  const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
+  Key llo = key_from_words<Key>(L.lut_lo), lhi = key_from_words<Key>(L.lut_hi);
+  if (llo < tlo) llo = tlo;
+  if (lhi > thi) lhi = thi;
+  if (lhi < llo) lhi = llo;
+  const bool span = (lhi - llo) >= ((thi - tlo) >> 2);
+  if (span) {
+    llo = tlo;
+    lhi = thi;
+  }
+  const int lbits = (int)L.lut_bits;
+  int ls = bitlen((Key)(lhi - llo)) - lbits;
+  if (ls < 0) ls = 0;
+  const u32 nlut = (u32)((lhi - llo) >> ls) + 1;
+  const int nspl = (1 << l) - 1;
+  const int eq = (int)L.equality;
+  __syncthreads();  // (all threads have read lut_lo / lut_hi)
+  if (threadIdx.x == 0) {
+    key_to_words<Key>(llo, L.lut_lo);
+    L.lut_ls = (u32)ls;
+    L.lut_n = nlut;
+    L.lut_span = span ? 1u : 0u;
+  }
+  auto lower = [&](Key v) -> u32 {  // #{spl[i] < v, i < s}
+    u32 a = 0, b = (u32)nspl;
+    while (a < b) {
+      const u32 mid = (a + b) >> 1;
+      if (cand[(int)mid < u ? (int)mid : u - 1] < v) a = mid + 1;
+      else b = mid;
+    }
+    return a;
+  };
+  unsigned short *lut = A.luts + L.lut_off;
+  for (u32 q = threadIdx.x; q < (1u << lbits); q += blockDim.x) {
+    u32 e = 0;
+    if (q < nlut) {
+      const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
+      const Key r1 = q + 1 == nlut ? thi : llo + (((Key)(q + 1)) << ls) - 1;
+      // a = #{splitters < r0}; the count covers splitters in [r0, r1] (a slot
+      // with none cannot hold a key equal to a splitter: key < s_a, except
+      // above the last splitter -- bucket 2s+1 with equality buckets)
+      const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
+      e = b == a ? LUT_FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | (min(b - a, 63u) << 9);
+    }
+    lut[q] = (unsigned short)e;
+  }
+}
+
 // Trees are stored as [tree[0..KIDX) | splitter[0..KIDX)] per task.
 template <int DT, int ALGO>
 __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
@@ -350,6 +406,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
     int rank = (2 * p + 1) * (1 << (l - 1 - d)) - 1;
     tree[i] = s_cand[rank < u ? rank : u - 1];
   }
+  if constexpr (Tr::D <= 16) build_lut<Key>(A, L, ti, s_cand, u, l);
   (void)s;
 }
 

@@ -114,17 +114,22 @@ def test_pointer_alignment_per_dtype(ips, orc):
 
 def test_level_with_more_than_65535_tasks(ips, orc):
     """A small base-case capacity forces > 65535 tasks at level 3 (the cleanup
-    grids are flattened; gridDim.y would cap them at 65535).  The arena, sized
-    for the first two levels, runs that level in several rounds."""
+    grids are flattened; gridDim.y would cap them at 65535).  A large arena
+    lets that level run as ONE round; with the default arena it runs in
+    several rounds."""
     import torch
 
     n = 1 << 25
     a = gen.uniform_u64(n, 21)
     t = to_dev(a)
-    st = ips.sort_ex(t, U64, base_cap=64)
+    st = ips.sort_ex(t, U64, base_cap=64, arena_mb=6144)
     g = from_dev(t, a)
-    assert sum(st["tasks_per_level"][2:]) > 65535, st["tasks_per_level"]
+    assert max(st["tasks_per_level"]) > 65535, st["tasks_per_level"]
     assert orc.parity(g, orc.sort(a, U64), U64) == -1
+    t.copy_(to_dev(a))
+    st = ips.sort_ex(t, U64, base_cap=64)
+    assert max(st["tasks_per_level"]) < 65536 and st["levels"] > 3, st["tasks_per_level"]
+    assert orc.parity(from_dev(t, a), orc.sort(a, U64), U64) == -1
     del t
     torch.cuda.empty_cache()
 
@@ -160,9 +165,9 @@ def test_rounds_defer_tasks_when_the_arena_is_full(ips, orc):
     a = a.astype(np.uint64)
     rng.shuffle(a)
     t = to_dev(a)
-    st = ips.sort_ex(t, U64, base_cap=128)
+    st = ips.sort_ex(t, U64, base_cap=128, arena_mb=1)  # the arena holds the root level only
     assert orc.parity(from_dev(t, a), orc.sort(a, U64), U64) == -1
-    assert st["levels"] >= 3
+    assert st["levels"] >= 3 and st["tasks_per_level"][1] < st["tasks_per_level"][0] * 256, st["tasks_per_level"]
 
 
 def test_device_status_word(ips):
