@@ -122,8 +122,10 @@ typedef struct ips4o_stats {
                                          (the scheduler runs inside 3), 8 base case,
                                          9 reverse, 10 device planner, 11 total device
                                          time of the sort (first start to last end)   */
-    uint64_t kernel_launches;         /* kernels launched by this call (1 by the host,
-                                         the rest by the device planner)              */
+    uint64_t kernel_launches;         /* kernels launched by this call (round 0 by the
+                                         host, the rest by the device planner)        */
+    uint64_t deferred_tasks;          /* tasks a round deferred because the arena was
+                                         full (they ran in a later round)             */
 } ips4o_stats;
 
 /* Sort the n elements at DEVICE pointer ptr ascending, in place, unstably,

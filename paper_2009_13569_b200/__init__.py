@@ -48,7 +48,7 @@ class Stats(ctypes.Structure):
         ("elems_per_level", ctypes.c_uint64 * MAX_LEVELS_REPORTED),
         ("basecase_tasks", ctypes.c_uint64), ("basecase_elems", ctypes.c_uint64),
         ("equal_elems", ctypes.c_uint64), ("kernel_ms", ctypes.c_float * 12),
-        ("kernel_launches", ctypes.c_uint64),
+        ("kernel_launches", ctypes.c_uint64), ("deferred_tasks", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
@@ -62,6 +62,7 @@ class Stats(ctypes.Structure):
             "equal_elems": int(self.equal_elems),
             "kernel_ms": {k: float(v) for k, v in zip(KERNEL_NAMES, self.kernel_ms)},
             "kernel_launches": int(self.kernel_launches),
+            "deferred_tasks": int(self.deferred_tasks),
         }
 
 

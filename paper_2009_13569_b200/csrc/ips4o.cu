@@ -277,6 +277,7 @@ static void fill_stats(const SortCtl &h, ips4o_stats *out, u64 scratch) {
   out->basecase_elems = (u64)h.counters[6] | ((u64)h.counters[7] << 32);
   out->equal_elems = (u64)h.counters[2] | ((u64)h.counters[3] << 32);
   out->kernel_launches = h.launches;
+  out->deferred_tasks = h.deferred;
   double fam[IPS4O_NUM_KERNELS] = {0};
   unsigned long long t0 = ~0ull, t1 = 0;
   for (int r = 0; r < MAX_ROUNDS; ++r)
