@@ -17,8 +17,10 @@ enum { ALGO_TREE = 0, ALGO_DIGIT = 1 };
 // Flags of a task.
 enum : u32 {
   TF_NONE = 0,
-  TF_MINMAX = 1,  // bounds unknown ([0, max]); K2 computes the key min/max and
-                  // K6 uses them for the children (the pre-pass was skipped)
+  TF_LOOSE = 1,   // [lo, hi] are valid bounds but may be loose (the root when the
+                  // pre-pass was skipped: [0, max]; K6 passes the flag on to the
+                  // children whose bound is the parent's); the base case measures
+                  // the exact key range of such a bucket before taking its digit
   TF_MEASURE = 2, // DIGIT: the parent's digit left more than half of it in this
                   // bucket; K0m measures the exact key range before the digit setup
 };
@@ -123,7 +125,6 @@ struct LevelArgs {
   u64 seed;
   u32 dbg_one_agent;          // debug: a single permutation agent per task
   u32 sample_p;               // K1 shared layout: sample slots (pow2 >= every task's m)
-  u64 *minmax;                // [0] = min key, [1] = max key of TF_MINMAX tasks (u64 keys)
   const u32 *measure_part;    // [2 * nmeasure_parts]: task, part | nparts << 16 (K0m)
   const u32 *measure_task;    // [3 * nmeasure]: task, first part, nparts (K0m)
   void *measure_out;          // [nmeasure_parts] PrepassPart: per-part key min/max

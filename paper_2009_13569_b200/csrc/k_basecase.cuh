@@ -378,6 +378,43 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     };
     const int m = (int)t.size;
     char *g = base + t.begin * (u64)D;
+    if constexpr (!BI::STAGE_RECORDS) {
+      if (t.flags & TF_LOOSE) {
+        // bounds inherited from a loose root bound (TF_LOOSE, an edge bucket
+        // of a sort whose pre-pass was skipped): measure the exact key range
+        // first, one extra read of the bucket, so that the digit below
+        // spreads the keys
+        __shared__ Key s_mm[2][NT / 32];
+        Key mn = key_max<Key>(), mx = (Key)0;
+        for (int i = tid; i < m; i += NT) {
+          const Key k = BI::key(BI::load(g + (size_t)i * D, (u32)i));
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const Key a = shfl_xor_key(mn, o), b = shfl_xor_key(mx, o);
+          mn = a < mn ? a : mn;
+          mx = b > mx ? b : mx;
+        }
+        if (lane == 0) {
+          s_mm[0][wid] = mn;
+          s_mm[1][wid] = mx;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < NT / 32; ++w) {
+            mn = s_mm[0][w] < mn ? s_mm[0][w] : mn;
+            mx = s_mm[1][w] > mx ? s_mm[1][w] : mx;
+          }
+          key_to_words<Key>(mn, s_task[cur].lo);
+          key_to_words<Key>(mx, s_task[cur].hi);
+          s_task[cur].flags &= ~(u32)TF_LOOSE;
+          digit_par(s_task[cur], s_par[cur]);
+        }
+        __syncthreads();
+      }
+    }
     const Key lo = key_from_words<Key>(t.lo), hi = key_from_words<Key>(t.hi);
     if (m <= 1 || !(lo < hi)) {
       publish_next();

@@ -399,8 +399,6 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     const uint4 *src = reinterpret_cast<const uint4 *>(A.luts + L.lut_off);
     for (u32 q = tid; q < (2u << L.lut_bits) / 16; q += NT) reinterpret_cast<uint4 *>(s_lut)[q] = src[q];
   }
-  const bool want_minmax = (L.t.flags & TF_MINMAX) != 0;
-  Key kmin = key_max<Key>(), kmax = (Key)0;
 
   const u64 n = s1 > s0 ? s1 - s0 : 0;
   unsigned short *const bidp = A.bid + L.blk_off + s0 / B;  // block buckets of this stripe (K4)
@@ -442,23 +440,6 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       Key key[IPT];
 #pragma unroll
       for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
-      if (want_minmax) {
-        if (cnt == T) {
-#pragma unroll
-          for (int k = 0; k < IPT; ++k) {
-            kmin = key[k] < kmin ? key[k] : kmin;
-            kmax = key[k] > kmax ? key[k] : kmax;
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < IPT; ++k) {
-            if (tid + k * NT < cnt) {
-              kmin = key[k] < kmin ? key[k] : kmin;
-              kmax = key[k] > kmax ? key[k] : kmax;
-            }
-          }
-        }
-      }
       if (ALGO == ALGO_TREE) {
         u32 ent[IPT];
 #pragma unroll
@@ -611,20 +592,6 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     const int f = (int)s_plan[j];
     Unit *dst = reinterpret_cast<Unit *>(A.partials + (sbase + j) * (u64)B * Tr::D);
     for (int u = lane; u < f; u += 32) dst[u] = s_buf[j * BUFS + u];
-  }
-  if constexpr (sizeof(Key) == 8) {
-    if (want_minmax) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        Key a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
-        kmin = a < kmin ? a : kmin;
-        kmax = b > kmax ? b : kmax;
-      }
-      if (lane == 0) {
-        atomicMin(reinterpret_cast<unsigned long long *>(&A.minmax[0]), (unsigned long long)kmin);
-        atomicMax(reinterpret_cast<unsigned long long *>(&A.minmax[1]), (unsigned long long)kmax);
-      }
-    }
   }
 }
 

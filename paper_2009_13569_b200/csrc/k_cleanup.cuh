@@ -147,13 +147,8 @@ __device__ void schedule_task(const LevelArgs &A, u32 ti, const u64 *sE) {
   constexpr int KI = Tr::KIDX;
   const LevelTask &L = A.tasks[ti];
   const int K = (int)L.K;
-  Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
-  if constexpr (sizeof(Key) == 8) {
-    if (L.t.flags & TF_MINMAX) {  // bounds measured by K2 (pre-pass skipped)
-      plo = (Key)A.minmax[0];
-      phi = (Key)A.minmax[1];
-    }
-  }
+  const Key plo = key_from_words<Key>(L.t.lo), phi = key_from_words<Key>(L.t.hi);
+  const bool loose = (L.t.flags & TF_LOOSE) != 0;
   const Key *gt = reinterpret_cast<const Key *>(A.trees) + (size_t)ti * 2 * KI;
   const Key *spl = gt + KI;
   for (int j = threadIdx.x; j < K; j += blockDim.x) {
@@ -208,10 +203,11 @@ __device__ void schedule_task(const LevelArgs &A, u32 ti, const u64 *sE) {
     key_to_words<Key>(lo, c.lo);
     key_to_words<Key>(hi, c.hi);
     c.level = L.t.level + 1;
-    c.flags = 0;
+    // a bound taken from a loose parent bound stays loose (TF_LOOSE)
+    c.flags = loose && (lo == plo || hi == phi) ? (u32)TF_LOOSE : 0u;
     // DIGIT: a digit that kept most of the task splits bits the keys do not
     // use (sparse keys); measure the child's exact range first (DESIGN R27)
-    if (ALGO == ALGO_DIGIT && 2 * sz > L.t.size) c.flags = TF_MEASURE;
+    if (ALGO == ALGO_DIGIT && 2 * sz > L.t.size) c.flags |= TF_MEASURE;
     u32 *cnt;
     TaskDesc *list;
     u32 cap;

@@ -15,37 +15,6 @@ struct PrepassPart {
   u64 mn[KEY_WORDS], mx[KEY_WORDS];
 };
 
-template <class Key>
-__device__ __forceinline__ Key shfl_key(Key v, int src) {
-  return __shfl_sync(0xffffffffu, v, src);
-}
-template <>
-__device__ __forceinline__ u128 shfl_key<u128>(u128 v, int src) {
-  u64 lo = __shfl_sync(0xffffffffu, (u64)v, src);
-  u64 hi = __shfl_sync(0xffffffffu, (u64)(v >> 64), src);
-  return ((u128)hi << 64) | lo;
-}
-template <>
-__device__ __forceinline__ K192 shfl_key<K192>(K192 v, int src) {
-  return K192(__shfl_sync(0xffffffffu, v.w[0], src), __shfl_sync(0xffffffffu, v.w[1], src),
-              __shfl_sync(0xffffffffu, v.w[2], src));
-}
-template <class Key>
-__device__ __forceinline__ Key shfl_xor_key(Key v, int m) {
-  return __shfl_xor_sync(0xffffffffu, v, m);
-}
-template <>
-__device__ __forceinline__ K192 shfl_xor_key<K192>(K192 v, int m) {
-  return K192(__shfl_xor_sync(0xffffffffu, v.w[0], m), __shfl_xor_sync(0xffffffffu, v.w[1], m),
-              __shfl_xor_sync(0xffffffffu, v.w[2], m));
-}
-template <>
-__device__ __forceinline__ u128 shfl_xor_key<u128>(u128 v, int m) {
-  u64 lo = __shfl_xor_sync(0xffffffffu, (u64)v, m);
-  u64 hi = __shfl_xor_sync(0xffffffffu, (u64)(v >> 64), m);
-  return ((u128)hi << 64) | lo;
-}
-
 // Each warp scans one contiguous segment in coalesced chunks of 32*V
 // elements (V consecutive elements per lane, read with 16-byte vector loads
 // when the array is 16-byte aligned); the right neighbour of a lane's last

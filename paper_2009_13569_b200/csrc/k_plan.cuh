@@ -194,7 +194,6 @@ template <int DT> __host__ __device__ u64 layout(LevelArgs &A, char *base, const
   A.rdone = reinterpret_cast<unsigned char *>(take(P.nblk));
   A.bid = reinterpret_cast<unsigned short *>(take(P.nblk * 2));
   A.task_done = reinterpret_cast<u32 *>(take(P.T * 4));
-  A.minmax = reinterpret_cast<u64 *>(take(16));
   A.measure_part = reinterpret_cast<const u32 *>(take(P.mparts * 8));
   A.measure_task = reinterpret_cast<const u32 *>(take(P.mtasks * 12));
   A.measure_out = take(P.mparts * sizeof(PrepassPart));
@@ -562,8 +561,6 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
     ctl->deferred += p - q;
     ctl->counters[1] = 0;
     ctl->counters[8] = 0;
-    A.minmax[0] = ~0ull;
-    A.minmax[1] = 0;
     if (r < MAX_ROUNDS) {
       ctl->tasks_per_round[r] = q;
       ctl->elems_per_round[r] = N;
@@ -711,11 +708,12 @@ __global__ void __launch_bounds__(PLAN_THREADS) entry_kernel(SortCfg cfg) {
   if (need_prepass && !c.capture && !c.skip_prepass && c.algo == ALGO_TREE && sizeof(Key) == 8 &&
       c.n > c.base_cap && c.n >= (1ull << 22)) {
     // cheap sample pre-check: an ascending and a descending sampled pair
-    // prove the input is not an easy input; the key range then comes from K2
+    // prove the input is not an easy input; the root's bounds are then the
+    // whole key space (TF_LOOSE: the base case measures edge buckets)
     const int f = presample_block<DT>(c.base, c.n);
     if (f == 3) {
       need_prepass = false;
-      flags = TF_MINMAX;
+      flags = TF_LOOSE;
     }
   }
 #ifdef IPS4O_PLAN_CLOCKS
@@ -729,7 +727,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) entry_kernel(SortCfg cfg) {
   TaskDesc root;
   memset(&root, 0, sizeof root);
   root.size = c.n;
-  root.flags = flags;
+  root.flags = flags | TF_LOOSE;  // bounds [0, max] (no pre-pass)
   key_to_words<Key>((Key)0, root.lo);
   key_to_words<Key>(key_max<Key>(), root.hi);
   start_rounds<DT, ALGO>(ctl, root);

@@ -179,7 +179,16 @@ __device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *c
       // with none cannot hold a key equal to a splitter: key < s_a, except
       // above the last splitter -- bucket 2s+1 with equality buckets)
       const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
-      e = b == a ? LUT_FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a) : a | (min(b - a, 63u) << 9);
+      if (b == a) {
+        e = LUT_FIN | (eq ? 2 * a + (a == (u32)nspl ? 1u : 0u) : a);
+      } else if (r0 == r1) {
+        // a slot of one key value that equals splitter s_a (b > a): its bucket
+        // is final too -- the equality bucket 2a+1, or a without equality
+        // buckets (s_{a-1} < r0 <= s_a); duplicate-heavy inputs
+        e = LUT_FIN | (eq ? 2 * a + 1 : a);
+      } else {
+        e = a | (min(b - a, 63u) << 9);
+      }
     }
     lut[q] = (unsigned short)e;
   }
