@@ -312,8 +312,10 @@ static int next_pow2_int(int x)
 /* P:728 "k-1 splitters are picked equidistantly from the sorted sample",
  * P:729 "we check for and remove duplicates", P:733 equality buckets "when
  * there are several identical splitters" (R23: at least one duplicate).
- * R10: with equality buckets on, 2*(s+1) bucket indices must fit kidx_max,
- * otherwise k is halved (alpha doubled) and the pick is repeated. */
+ * R10: with equality buckets on, 2*(s+1) bucket indices must fit kidx_max.
+ * If at most max(1, (kidx_max/2 - 1)/8) unique splitters are too many, only
+ * the kidx_max/2 - 1 picked most often stay (ties: the smaller first), k
+ * unchanged; otherwise k is halved (alpha doubled) and the pick repeated. */
 int orc_select_splitters(const void *sorted_sample, uint64_t m, int k, int kidx_max,
                          int dtype, void *out_splitters, int *equality, int *k_final)
 {
@@ -324,17 +326,42 @@ int orc_select_splitters(const void *sorted_sample, uint64_t m, int k, int kidx_
         uint64_t alpha = m / (uint64_t)k;
         int u = 0;
         int dup = 0;
+        int picks[512];          /* picks per unique splitter (k <= 512) */
         for (int j = 0; j < k - 1; j++) {
             const unsigned char *c = S + ((uint64_t)(j + 1) * alpha - 1) * D;
             if (u > 0 && equal_keys(dtype, out + (size_t)(u - 1) * D, c)) {
                 dup = 1;
+                picks[u - 1]++;
                 continue;
             }
             memcpy(out + (size_t)u * D, c, D);
+            picks[u] = 1;
             u++;
         }
         int leaves = next_pow2_int(u + 1);
         int need = dup ? 2 * leaves : leaves;
+        int keep_n = kidx_max / 2 - 1;
+        int slack = keep_n / 8 > 1 ? keep_n / 8 : 1;
+        if (dup && need > kidx_max && kidx_max >= 4 && u - keep_n <= slack) {
+            /* DESIGN R10: keep the kidx_max/2 - 1 unique splitters with the
+             * most picks; among equal pick counts the smaller ones first.
+             * Written as the definition: a splitter stays iff fewer than
+             * kidx_max/2 - 1 splitters rank before it in the order (more
+             * picks first, then smaller index). */
+            int w = 0;
+            for (int i = 0; i < u; i++) {
+                int before = 0;
+                for (int j = 0; j < u; j++)
+                    if (picks[j] > picks[i] || (picks[j] == picks[i] && j < i)) before++;
+                if (before < keep_n) {
+                    memmove(out + (size_t)w * D, out + (size_t)i * D, D);
+                    w++;
+                }
+            }
+            u = w;
+            leaves = next_pow2_int(u + 1);
+            need = 2 * leaves;
+        }
         if (need <= kidx_max || k <= 2) {
             *equality = dup;
             *k_final = k;

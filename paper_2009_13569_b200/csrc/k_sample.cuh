@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   u32 *s_hist = reinterpret_cast<u32 *>(smem_raw + (size_t)A.sample_p * sizeof(Key));
   const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);
   __shared__ Key s_cand[256], s_pick[256], s_red[2][32];
+  __shared__ int s_wt[256];  // picks per unique splitter (R10)
   __shared__ u32 s_ws[SAMPLE_THREADS / 32 + 1];
   __shared__ int s_u, s_leaves, s_k, s_slow;
   Key *tree = reinterpret_cast<Key *>(A.trees) + (size_t)ti * 2 * Tr::KIDX;
@@ -342,7 +343,8 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
     s_k = (int)L.k_req;
   }
   // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
-  // duplicate was removed (R23); R10: halve k until the indices fit.
+  // duplicate was removed (R23); R10: keep the most-picked equality
+  // splitters that fit the index budget (halve k otherwise).
   bool sorted = false;
   for (;;) {
     __syncthreads();
@@ -377,12 +379,44 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
         const Key c = s_pick[j];
         if (u > 0 && s_cand[u - 1] == c) {
           dup = 1;
+          ++s_wt[u - 1];
           continue;
         }
+        s_wt[u] = 1;
         s_cand[u++] = c;
       }
-      const int leaves = next_pow2_i(u + 1);
-      const int need = dup ? 2 * leaves : leaves;
+      int leaves = next_pow2_i(u + 1);
+      int need = dup ? 2 * leaves : leaves;
+      const int up = (int)L.kidx / 2 - 1;
+      if (dup && need > (int)L.kidx && L.kidx >= 4 && u - up <= (up / 8 > 1 ? up / 8 : 1)) {
+        // R10: the bucket indices of u equality splitters exceed the budget by
+        // a few splitters: keep the kidx/2 - 1 picked most often (the
+        // heaviest keys keep their equality buckets), ties by rank; k is
+        // unchanged.  (More to drop: halve k below, which keeps the
+        // splitters evenly spread.)
+        auto at_least = [&](int w) {
+          int c = 0;
+          for (int i = 0; i < u; ++i) c += s_wt[i] >= w ? 1 : 0;
+          return c;
+        };
+        int lo = 1, hi = k;  // largest T with #{wt >= T} >= up
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (at_least(mid) >= up) lo = mid;
+          else hi = mid - 1;
+        }
+        const int T = lo;
+        int take = up - at_least(T + 1);
+        int w = 0;
+        for (int i = 0; i < u; ++i) {
+          const bool keep = s_wt[i] > T || (s_wt[i] == T && take > 0);
+          if (s_wt[i] == T && keep) --take;
+          if (keep) s_cand[w++] = s_cand[i];
+        }
+        u = w;
+        leaves = next_pow2_i(u + 1);
+        need = 2 * leaves;
+      }
       if (need <= (int)L.kidx || k <= 2) {
         L.K = (u32)need;
         L.l = (u32)log2_i(leaves);

@@ -385,8 +385,11 @@ def test_classifier_f64_and_rec100_use_the_dtype_order(orc):
 
 
 def test_select_splitters_equality_budget(orc):
-    """R10: with duplicates among 255 candidates and a 256-index budget the
-    pick is repeated with k/2 (127 candidates, so 2*128 indices fit)."""
+    """R10: 255 picks from a sample with 200 zeros give 1 + 205 unique
+    splitters; 2*256 indices do not fit 256 and 79 are too many to thin away
+    (more than 127/8), so the pick is repeated with k/2 (127 candidates).  With
+    128 unique splitters (1 over the budget) the 127 picked most often stay:
+    the heaviest keys keep their equality buckets, ties keep the smaller."""
     m = 256 * 4
     sample = np.sort(np.concatenate([np.zeros(200, dtype=np.uint64),
                                      np.arange(1, m - 199, dtype=np.uint64)]))
@@ -395,6 +398,11 @@ def test_select_splitters_equality_budget(orc):
     u = sp.size // 8
     leaves = 1 << math.ceil(math.log2(u + 1))
     assert 2 * leaves <= 256
+    # 128 unique picks (one over the budget): 0 picked 128 times, 1..127 once each
+    s2 = np.sort(np.concatenate([np.zeros(512, dtype=np.uint64), np.repeat(np.arange(1, 129, dtype=np.uint64), 4)]))
+    sp3, eq3, kf3 = orc.select_splitters(s2, 256, 256, U64)
+    got = sp3.view(np.uint64).tolist()
+    assert eq3 and kf3 == 256 and got == list(range(0, 127)), got
     sp2, eq2, kf2 = orc.select_splitters(np.arange(m, dtype=np.uint64), 256, 256, U64)
     assert kf2 == 256 and not eq2 and sp2.size // 8 == 255
 
