@@ -7,12 +7,15 @@ on B200 (BASELINE.json metric), plus the HBM roofline of the dominant kernel.
 
 One step = one full ips4o_sort of the whole array (all SURVEY 8(a) rows:
 pre-pass, sampling, classification, boundaries, stripe fix, permutation,
-cleanup, scheduling, base case) on inputs already resident in HBM.  Before
-every step (outside the timed region) the working array is restored from a
-pristine device copy; the 8 GiB input is far larger than the 126 MB L2, so no
-extra L2 flush is needed.  Timing: CUDA events on the sorting stream,
-bracketed by barrier + synchronize; max over ranks.  N > 1 runs independent
-replicas (DESIGN "Multi-GPU: replicas only"), weak scaling.
+cleanup, scheduling, base case; the levels are planned and launched by the
+device) on inputs already resident in HBM.  Before every step (outside the
+timed region) the working array is restored from a pristine device copy; the
+8 GiB input is far larger than the 126 MB L2, so no extra L2 flush is needed.
+Timing: CUDA events on the sorting stream around the asynchronous ips4o_sort,
+bracketed by barrier + synchronize; max over ranks.  The per-kernel times
+(roofline) come from separate untimed steps with device timing stamps
+(ips4o_stats, opt.timing).  N > 1 runs independent replicas (DESIGN
+"Multi-GPU: replicas only"), weak scaling.
 """
 from __future__ import annotations
 
@@ -46,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-log2", type=int, default=25, help="oracle sample size (log2)")
+    ap.add_argument("--stat-steps", type=int, default=3, help="untimed steps with per-kernel device timing")
+    ap.add_argument("--no-c1", action="store_true", help="skip the c1 (2^20) hot/cold-L2 extra")
     return ap.parse_args()
 
 
@@ -111,9 +116,13 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+NOMINAL_HBM_GBS = 8000.0  # BASELINE.json's "~8 TB/s" contract
+
+
 def ncu_traffic():
-    """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """DRAM bytes per step of each kernel family from the committed ncu launch
+    list of the same workload (profiles/r2_ncu_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
     if os.path.exists(p):
         try:
             return json.load(open(p))
@@ -147,10 +156,14 @@ def cpu_baseline(dist: str, log2n: int, seed: int) -> dict:
     t0 = time.perf_counter()
     oracle.sort_inplace(a, dt)
     t = time.perf_counter() - t0
+    full = 1 << 30
     return {"value": n / t / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
             "sample": f"first 2^{log2n} keys of the {dist} stream (seed {seed}), "
                       f"single-threaded top-down mergesort, {t:.2f} s",
-            "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+            # a mergesort's time grows as n log n: the rate at 2^30 estimated
+            # from the sample (the sample itself is what was measured)
+            "value_at_2p30_nlogn_estimate": n / t / 1e9 * log2n / 30.0,
+            "host_cpu": _cpu_model(), "nproc": os.cpu_count(), "threads_used": 1, "full_n": full}
 
 
 def _cpu_model():
@@ -182,6 +195,40 @@ def aggregate_value(n_per_rank: int, world: int, steps: int, max_total_ms: float
     """Whole-job Gkeys/s: every rank sorts its own n keys per step (replicas,
     weak scaling); time = max over ranks."""
     return world * n_per_rank * steps / (max_total_ms / 1e3) / 1e9
+
+
+def c1_hot_cold(ips, dev, stream, reps: int = 10) -> dict:
+    """BASELINE config 1 (2^20 uint64 Uniform, seed 1; 8 MiB, L2-resident):
+    device time per sort with the input hot in L2 (sorted back to back) and
+    cold (L2 flushed by writing a 512 MiB buffer before every rep)."""
+    import numpy as np
+    import torch
+
+    import synth_inputs as gen
+
+    n = 1 << 20
+    src = torch.from_numpy(gen.uniform_u64(n, 1).view(np.int64)).to(dev)
+    work = torch.empty_like(src)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for mode in ("hot", "cold"):
+        ts = []
+        for r in range(reps + 2):
+            work.copy_(src)
+            if mode == "cold":
+                flush.fill_(r & 0xFF)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ips.sort(work, 0)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1))
+        out[mode] = {"ms": statistics.mean(ts), "min_ms": min(ts), "Gkeys_s": n / (statistics.mean(ts) / 1e3) / 1e9}
+    out["workload"] = "c1: 2^20 uint64 Uniform (seed 1), 8 MiB"
+    del flush
+    return out
 
 
 def dist_dtype(dist: str) -> int:
@@ -256,7 +303,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        st = ips.sort_ex(work, dt, algo=algo, timing=True) if stats else ips.sort(work, dt, algo=algo)
+        if stats:  # synchronises inside (reads the device control block back)
+            st = ips.sort_ex(work, dt, algo=algo, timing=True)
+        else:      # the asynchronous product call: one stream-ordered enqueue
+            st = ips.sort(work, dt, algo=algo)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         return ev0.elapsed_time(ev1), st
@@ -270,11 +320,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize(dev)
     clk = ClockSampler(local_rank)
     clk.start()
-    times, stats = [], []
+    times = []
     for _ in range(args.steps):
-        t, st = one_step(True)
+        t, _ = one_step(False)
         times.append(t)
-        stats.append(st)
     torch.cuda.synchronize(dev)
     clocks = clk.stop()
     total_ms = max_over_ranks(sum(times), dev)
@@ -282,6 +331,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         import torch.distributed as dist
 
         dist.barrier()
+    # per-kernel device times (globaltimer stamps) from separate untimed steps
+    stats = [one_step(True)[1] for _ in range(args.stat_steps)]
     # correctness guard on the last result (cheap, on device): non-decreasing
     chk_ok = None
     if dt == 0:
@@ -309,9 +360,28 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = ncu_traffic()
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak if achieved else None,
-            "traffic": (traffic or {}).get(dom), "traffic_unit": "DRAM bytes per step (ncu, profiles/ncu_traffic.json)",
+            "frac_of_nominal_8000": achieved / NOMINAL_HBM_GBS if achieved else None,
+            "traffic": (traffic or {}).get(dom), "traffic_unit": "DRAM bytes per step (ncu, profiles/r2_ncu_traffic.json)",
             "peak_source": peak_src,
-            "alg_bytes_per_step": alg[dom], "kernel_ms_per_step": km[dom]}
+            "alg_bytes_per_step": alg[dom], "kernel_ms_per_step": km[dom],
+            "timing": "device globaltimer stamps per kernel (earliest CTA start to latest warp end), "
+                      f"mean of {len(stats)} untimed steps"}
+    # per level and per pass: algorithmic GB/s of the partition passes
+    levels = []
+    for r, rk in enumerate(st.get("round_kernel_ms", [])):
+        ne = st["elems_per_level"][r]
+        row = {"level": r + 1, "tasks": st["tasks_per_level"][r], "elems": ne}
+        for k in ("classify", "permute"):
+            ms = statistics.mean(s["round_kernel_ms"][r][k] for s in stats)
+            gbs = 2 * D * ne / (ms / 1e3) / 1e9 if ms else None
+            row[k] = {"ms": ms, "alg_GBps": gbs, "frac": gbs / peak if gbs else None,
+                      "frac_of_nominal_8000": gbs / NOMINAL_HBM_GBS if gbs else None}
+        levels.append(row)
+    bms = km.get("basecase", 0)
+    base_row = {"ms": bms, "alg_GBps": alg["basecase"] / (bms / 1e3) / 1e9 if bms else None}
+    if base_row["alg_GBps"]:
+        base_row["frac"] = base_row["alg_GBps"] / peak
+        base_row["frac_of_nominal_8000"] = base_row["alg_GBps"] / NOMINAL_HBM_GBS
     # algorithmic whole-sort reading: 2 n D per partition level (+ base case)
     L_eff = elems_levels / n
     sort_ms = total_ms / args.steps
@@ -319,7 +389,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                  "frac_partition_2nDL": (2 * n * D * L_eff / (peak * 1e9)) / (
                      (km["classify"] + km["permute"] + km["stripe_fix"] + km["cleanup"] + km["sample"]
                       + km["boundaries"] + km["schedule"]) / 1e3) if L_eff else None,
-                 "frac_sort_2nD_L_plus_1": (2 * n * D * (L_eff + 1) / (peak * 1e9)) / (sort_ms / 1e3)}
+                 "frac_sort_2nD_L_plus_1": (2 * n * D * (L_eff + 1) / (peak * 1e9)) / (sort_ms / 1e3),
+                 "frac_sort_2nD_L_plus_1_of_nominal_8000": (2 * n * D * (L_eff + 1) / (NOMINAL_HBM_GBS * 1e9)) / (sort_ms / 1e3),
+                 "per_level": levels, "basecase": base_row}
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         pin = torch.empty(n * D, dtype=torch.uint8).pin_memory()
@@ -336,6 +408,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         e2e = {"value": n * len(et) / sum(et) / 1e9, "unit": "Gkeys/s",
                "h2d_bytes_per_step": n * D, "d2h_bytes_per_step": n * D,
                "path": "ips4o_sort_host (pinned host buffer; H2D + sort + D2H inside the call)"}
+    c1 = None
+    if not args.no_c1 and dt == 0 and args.n >= 20:
+        c1 = c1_hot_cold(ips, dev, stream)
     cpu = None
     if not args.no_cpu:
         cpu = cpu_baseline(args.dist, min(args.cpu_log2, args.n), args.seed)
@@ -351,10 +426,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": roof, "roofline_sort": roof_sort,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        # kernels launched per sort (round 0 by the host, later rounds by the
+        # device planner; counted by the library) x timed steps
+        "gpu_launches": int(st["kernel_launches"]) * args.steps,
+        "gpu_launches_per_step": int(st["kernel_launches"]),
         "kernel_ms_per_step": km, "levels": st["levels"], "tasks_per_level": st["tasks_per_level"],
         "basecase_tasks": st["basecase_tasks"], "scratch_bytes": st["scratch_bytes"],
-        "sorted_check": chk_ok, "step_ms": times,
+        "sorted_check": chk_ok, "step_ms": times, "c1_l2": c1,
     }
     print(json.dumps(line), flush=True)
 

@@ -126,6 +126,9 @@ typedef struct ips4o_stats {
                                          host, the rest by the device planner)        */
     uint64_t deferred_tasks;          /* tasks a round deferred because the arena was
                                          full (they ran in a later round)             */
+    float round_kernel_ms[IPS4O_MAX_LEVELS_REPORTED][4]; /* per round, when opt->timing:
+                                         0 classify, 1 permute, 2 base case (+ split),
+                                         3 every other kernel of the round            */
 } ips4o_stats;
 
 /* Sort the n elements at DEVICE pointer ptr ascending, in place, unstably,

@@ -49,6 +49,7 @@ class Stats(ctypes.Structure):
         ("basecase_tasks", ctypes.c_uint64), ("basecase_elems", ctypes.c_uint64),
         ("equal_elems", ctypes.c_uint64), ("kernel_ms", ctypes.c_float * 12),
         ("kernel_launches", ctypes.c_uint64), ("deferred_tasks", ctypes.c_uint64),
+        ("round_kernel_ms", (ctypes.c_float * 4) * MAX_LEVELS_REPORTED),
     ]
 
     def as_dict(self) -> dict:
@@ -63,6 +64,8 @@ class Stats(ctypes.Structure):
             "kernel_ms": {k: float(v) for k, v in zip(KERNEL_NAMES, self.kernel_ms)},
             "kernel_launches": int(self.kernel_launches),
             "deferred_tasks": int(self.deferred_tasks),
+            "round_kernel_ms": [dict(zip(("classify", "permute", "basecase", "other"),
+                                         (float(x) for x in self.round_kernel_ms[r]))) for r in range(lv)],
         }
 
 

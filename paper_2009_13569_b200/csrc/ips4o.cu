@@ -289,6 +289,13 @@ static void fill_stats(const SortCtl &h, ips4o_stats *out, u64 scratch) {
       t1 = std::max(t1, b);
     }
   for (int i = 0; i < KF_TOTAL; ++i) out->kernel_ms[i] = (float)fam[i];
+  for (int r = 0; r < IPS4O_MAX_LEVELS_REPORTED && r < MAX_ROUNDS; ++r)
+    for (int k = 0; k < KS_COUNT; ++k) {
+      const unsigned long long a = h.tslot[r][k][0], b = h.tslot[r][k][1];
+      if (a == ~0ull || b < a) continue;
+      const int c = k == KS_CLASSIFY ? 0 : k == KS_PERM ? 1 : (k == KS_BASE || k == KS_SPLIT) ? 2 : 3;
+      out->round_kernel_ms[r][c] += (float)((double)(b - a) * 1e-6);
+    }
   out->kernel_ms[KF_TOTAL] = t1 > t0 ? (float)((double)(t1 - t0) * 1e-6) : 0.f;
 }
 

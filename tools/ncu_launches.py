@@ -17,7 +17,7 @@ FAMILY = [
     ("prepass", r"prepass"), ("sample", r"sample_kernel"), ("classify", r"classify"),
     ("boundaries", r"boundaries"), ("stripe_fix", r"stripe_fix"), ("permute", r"permute"),
     ("cleanup", r"cleanup"), ("schedule", r"schedule"), ("basecase", r"basecase"),
-    ("reverse", r"reverse"),
+    ("reverse", r"reverse"), ("plan", r"entry_kernel|driver_kernel"),
 ]
 
 
@@ -44,7 +44,8 @@ def main():
         v = float(r[I["Metric Value"]].replace(",", ""))
         d[r[I["Metric Name"]]] = v
     ids = list(launches)
-    starts = [i for i in ids if re.search(r"presample_kernel|prepass_kernel", launches[i]["name"])]
+    starts = [i for i in ids if re.search(r"entry_kernel", launches[i]["name"])] or \
+        [i for i in ids if re.search(r"presample_kernel|prepass_kernel", launches[i]["name"])]
     sel = ids[starts[-a.steps]:] if len(starts) >= a.steps else ids
     fam = defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_read": 0.0, "dram_write": 0.0})
     for i in sel:
