@@ -65,7 +65,7 @@ class Stats(ctypes.Structure):
             "kernel_launches": int(self.kernel_launches),
             "deferred_tasks": int(self.deferred_tasks),
             "round_kernel_ms": [dict(zip(("classify", "permute", "basecase", "other"),
-                                         (float(x) for x in self.round_kernel_ms[r]))) for r in range(lv)],
+                                         (float(x) for x in self.round_kernel_ms[r]))) for r in range(min(lv, MAX_LEVELS_REPORTED))],
         }
 
 

@@ -325,6 +325,16 @@ __device__ __forceinline__ int tile_load_async(char *s, const char *g, u64 nbyte
   return head;
 }
 
+// ------------------------------------------------------------------ checked build
+// IPS4O_CHECKS: every guarded index is bounds-checked on the device; a failed
+// check skips the access and raises ERR_CHECK (reported by the synchronising
+// calls and ips4o_device_status).  Without it the guard is `true` (no code).
+#ifdef IPS4O_CHECKS
+#define IPS4O_GUARD(cond, errp) ((cond) ? true : (atomicOr((errp), (u32)ERR_CHECK), false))
+#else
+#define IPS4O_GUARD(cond, errp) true
+#endif
+
 // ------------------------------------------------------------------ key shuffles
 template <class Key>
 __device__ __forceinline__ Key shfl_key(Key v, int src) {

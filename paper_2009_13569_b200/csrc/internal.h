@@ -148,6 +148,7 @@ enum : u32 {
   ERR_NO_PROGRESS = 4,    // a child task equal to its parent (dropped, never looped on)
   ERR_LAUNCH = 8,         // a device-side kernel launch failed
   ERR_ARENA = 16,         // a single task does not fit the level arena
+  ERR_CHECK = 32,         // checked build (IPS4O_CHECKS): an index failed its bounds check
 };
 
 // Device timing slots (globaltimer, ns) per round: [slot][0] = earliest CTA

@@ -261,6 +261,7 @@ static const char *err_text(u32 f) {
   if (f & ERR_NO_PROGRESS) return "internal error: a task made no progress";
   if (f & ERR_LAUNCH) return "a device-side kernel launch failed";
   if (f & ERR_ARENA) return "a task does not fit the scratch arena";
+  if (f & ERR_CHECK) return "checked build: an index failed its bounds check";
   return "device error";
 }
 

@@ -642,7 +642,8 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
               if (!SPLITK || (int)d < dsplit) {
                 const int sh = (d & 1) << 4;
                 const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
-                s_items[(old >> sh) & 0xFFFFu] = it[u];
+                if (IPS4O_GUARD(((old >> sh) & 0xFFFFu) < (u32)(m < BI::CAP ? m : BI::CAP), sp.err))
+                  s_items[(old >> sh) & 0xFFFFu] = it[u];
               } else {
                 scratch[atomicAdd(&s_scnt, 1u)] = it[u];
               }
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         }
         const int pos = off + a + rank;
         if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
-          reinterpret_cast<Item *>(g)[pos] = it;
+          if (IPS4O_GUARD(pos >= 0 && pos < m, sp.err)) reinterpret_cast<Item *>(g)[pos] = it;
         } else if constexpr (DT == DT_F64) {
           reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
         } else {

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(Traits<DT>::CLS_THREADS, 1) classify_kernel(Le
       const u32 bf = s_fill[j];
       const u32 eo = s_eoff[j];
       Unit *dst = reinterpret_cast<Unit *>(gtask + (s0 + (front + s_boff[j] + q) * B) * D);
+      if (!IPS4O_GUARD(s0 + (front + s_boff[j] + q + 1) * B <= s1, A.err)) continue;
       if (lane == 0) A.bid[L.blk_off + s0 / B + front + s_boff[j] + q] = (unsigned short)j;
       for (int u = lane; u < B * UPE; u += 32) {
         const int e = u / UPE, w = u - e * UPE;
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     // ---- the previous tile's leftovers enter their buffers
 #pragma unroll
     for (int k = 0; k < IPT; ++k)
-      if (sl[k] != NONE) s_buf[sl[k]] = xl[k];
+      if (sl[k] != NONE && IPS4O_GUARD(sl[k] < (u32)(KI * BUFS), A.err)) s_buf[sl[k]] = xl[k];
 
     // ---- plan: nb blocks per bucket; scan of (nb | staged blocks << 16)
     u32 nb = 0, boff = 0, soff = 0;
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       const u32 cut = (pl >> 8) & 0x1FFFu;
       const u32 pos = v < (u32)B ? j * BUFS + v : STG0 + (pl >> 21) * B + v - B;
       const bool keep = v < cut || v < (u32)B;
-      if (valid && keep) s_buf[pos] = x[k];
+      if (valid && keep && IPS4O_GUARD(pos < STG0 + (u32)T, A.err)) s_buf[pos] = x[k];
       sl[k] = (valid && !keep) ? j * BUFS + (v - cut) : NONE;
       xl[k] = x[k];
     }
@@ -559,6 +560,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
         const u32 j = jq & 0x1FFu, q = jq >> 9;
         const Unit *src = q == 0 ? s_buf + j * BUFS : s_stage + ((s_plan[j] >> 21) + q - 1) * B;
         Unit *dst = gtask + s0 + (front + g) * B;
+        if (!IPS4O_GUARD(s0 + (front + g + 1) * B <= s1, A.err)) continue;  // blocks stay in the stripe
 #pragma unroll
         for (int e = 0; e < B / 16; ++e) dst[hl + 16 * e] = src[hl + 16 * e];
       }
@@ -576,7 +578,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   __syncthreads();  // the last copies have read the buffers
 #pragma unroll
   for (int k = 0; k < IPT; ++k)
-    if (sl[k] != NONE) s_buf[sl[k]] = xl[k];
+    if (sl[k] != NONE && IPS4O_GUARD(sl[k] < (u32)(KI * BUFS), A.err)) s_buf[sl[k]] = xl[k];
   __syncthreads();
 
   // ---- outputs: counts, partial fill, full blocks, partial buffers

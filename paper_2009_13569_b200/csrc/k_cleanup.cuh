@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(CLN_WARPS * 32) cleanup_save_kernel(LevelArgs 
   };
   if (W > o0) {
     const u64 o = W - o0;  // < b
+    if (!IPS4O_GUARD(o < (u64)B, A.err)) return;
     Unit *dst = reinterpret_cast<Unit *>(A.overlap + (bo + j) * (u64)B * D);
     for (u64 u = lane; u < o * UPE; u += 32) {
       u64 e = u / UPE, w = u % UPE;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
       const Unit *src = reinterpret_cast<const Unit *>(A.overlap + (bo + j) * (u64)B * D);
       for (u64 u = lane; u < o * UPE; u += 32) {
         const u64 e = u / UPE, w = u % UPE;
-        reinterpret_cast<Unit *>(gtask + hole(e) * D)[w] = src[u];
+        if (IPS4O_GUARD(hole(e) < E1 && hole(e) >= E0, A.err)) reinterpret_cast<Unit *>(gtask + hole(e) * D)[w] = src[u];
       }
     }
     if (f == 0) continue;
@@ -126,7 +127,8 @@ __global__ void __launch_bounds__(FILL_THREADS) cleanup_fill_kernel(LevelArgs A)
     const Unit *src = reinterpret_cast<const Unit *>(A.partials + slot * (u64)B * D);
     for (u32 u = lane; u < f * UPE; u += 32) {
       const u32 e = u / UPE, w = u % UPE;
-      reinterpret_cast<Unit *>(gtask + hole(h0 + e) * D)[w] = src[u];
+      if (IPS4O_GUARD(hole(h0 + e) < E1 && hole(h0 + e) >= E0, A.err))
+        reinterpret_cast<Unit *>(gtask + hole(h0 + e) * D)[w] = src[u];
     }
   }
 }

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(FIX_THREADS) stripe_fix_kernel(LevelArgs A) {
       const u64 q = Fr1 - 1 - (skip + i);
       const u64 src = select(q);
       const u64 dstb = h0 + i;
+      if (!IPS4O_GUARD(src < nblk_total && dstb < nblk_total && (dstb + 1) * B <= L.t.size, A.err)) continue;
       const Unit *s = reinterpret_cast<const Unit *>(gtask + src * B * D);
       Unit *d = reinterpret_cast<Unit *>(gtask + dstb * B * D);
       for (int u = lane; u < NU; u += 32) d[u] = s[u];
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(PERM_THREADS, IPS4O_PERM_MINB) permute_kernel(
       }
     };
     auto store_blk = [&](u64 x, const Unit(&r)[NPL]) {
+      if (!IPS4O_GUARD(x < (size + B - 1) / B, A.err)) return;  // block positions of the task
       Unit *d = blk_ptr(x);
 #pragma unroll
       for (int i = 0; i < NPL; ++i) {
