@@ -194,6 +194,50 @@ typedef struct ips4o_dtype_info {
 } ips4o_dtype_info;
 int ips4o_get_dtype_info(int dtype, ips4o_dtype_info *out);
 
+/* ---------------------------------------------------------------- distributed samplesort
+ * The three local steps of the multi-GPU samplesort (the paper
+ * names IPS4o as the local step of distributed-memory sorting, P:3952-3953;
+ * the splitter rule is the paper's own).  One process per GPU;
+ * the exchange of samples and buckets between the GPUs is NCCL's (the Python
+ * package paper_2009_13569_b200.distributed composes the calls):
+ *   1. ips4o_sample              m samples of the local shard;
+ *   2. (all-gather of the samples) ips4o_select_splitters: p - 1 splitters;
+ *   3. ips4o_partition_splitters in-place partition of the shard into p ranges;
+ *   4. (all-to-all of the ranges) ips4o_sort of the received elements.
+ *
+ * ips4o_sample: writes m elements of the DEVICE array ptr[0..n) to DEVICE
+ * pointer out[0..m): out[j] = ptr[i_j] with i_j the counter-based draw of
+ * DESIGN R8 for the task (level 0, begin 0, size n) and `seed` (use a
+ * different seed per rank).  Sampling with replacement.
+ * Asynchronous on `stream`.  ptr and out need 4-byte alignment.
+ * Errors: IPS4O_ERR_INVALID (unknown dtype, n = 0 with m > 0, NULL pointers);
+ * m = 0 does nothing. */
+int ips4o_sample(const void *ptr, uint64_t n, int dtype, void *stream,
+                 uint64_t m, uint64_t seed, void *out);
+
+/* ips4o_select_splitters: sorts the DEVICE array samples[0..total) in place
+ * (ips4o_sort) and writes the parts - 1 equidistant picks
+ * out[j] = samples[((j + 1) * total) / parts - 1], j < parts - 1, to DEVICE
+ * pointer out.  Asynchronous.  parts = 1 does nothing; total < parts is
+ * IPS4O_ERR_INVALID. */
+int ips4o_select_splitters(void *samples, uint64_t total, int dtype, void *stream,
+                           int parts, void *out);
+
+/* ips4o_partition_splitters: partitions the DEVICE array ptr[0..n) in place
+ * into nspl + 1 ranges by the nspl given splitters S_0 <= ... <= S_{nspl-1}
+ * (DEVICE pointer, elements of `dtype`, sorted ascending by key): range r =
+ * [bounds[r], bounds[r+1]) holds the elements e with S_{r-1} < e <= S_r (S_-1
+ * = -inf, S_nspl = +inf; the bucket rule of P:392-394).  One partitioning
+ * step (sampling replaced by the given splitters; branchless tree with
+ * equality buckets when splitters repeat, block permutation, cleanup; no
+ * recursion), so each range is NOT sorted.  bounds is a HOST array of
+ * nspl + 2 uint64.  Synchronous (the caller needs the range sizes for the
+ * exchange).  1 <= nspl <= kidx_max/2 - 1 (127 for 8/16-byte elements).
+ * Errors: IPS4O_ERR_INVALID (bad arguments, splitters not sorted),
+ * IPS4O_ERR_NOMEM, IPS4O_ERR_CUDA. */
+int ips4o_partition_splitters(void *ptr, uint64_t n, int dtype, void *stream,
+                              const void *splitters, int nspl, uint64_t *bounds);
+
 /* ---------------------------------------------------------------- test hooks
  * One partitioning step (Sec. 4.1: sampling, classification,
  * block permutation, cleanup) over the whole array A[0..n), with NO recursion

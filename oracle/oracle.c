@@ -313,9 +313,10 @@ static int next_pow2_int(int x)
  * P:729 "we check for and remove duplicates", P:733 equality buckets "when
  * there are several identical splitters" (R23: at least one duplicate).
  * R10: with equality buckets on, 2*(s+1) bucket indices must fit kidx_max.
- * If at most max(1, (kidx_max/2 - 1)/8) unique splitters are too many, only
- * the kidx_max/2 - 1 picked most often stay (ties: the smaller first), k
- * unchanged; otherwise k is halved (alpha doubled) and the pick repeated. */
+ * If u unique splitters are too many, u - (kidx_max/2 - 1) of them are
+ * dropped, fewest picks first (ties: the smaller), never two neighbours, k
+ * unchanged; if that many cannot be dropped, k is halved (alpha doubled) and
+ * the pick repeated. */
 int orc_select_splitters(const void *sorted_sample, uint64_t m, int k, int kidx_max,
                          int dtype, void *out_splitters, int *equality, int *k_final)
 {
@@ -341,26 +342,37 @@ int orc_select_splitters(const void *sorted_sample, uint64_t m, int k, int kidx_
         int leaves = next_pow2_int(u + 1);
         int need = dup ? 2 * leaves : leaves;
         int keep_n = kidx_max / 2 - 1;
-        int slack = keep_n / 8 > 1 ? keep_n / 8 : 1;
-        if (dup && need > kidx_max && kidx_max >= 4 && u - keep_n <= slack) {
-            /* DESIGN R10: keep the kidx_max/2 - 1 unique splitters with the
-             * most picks; among equal pick counts the smaller ones first.
-             * Written as the definition: a splitter stays iff fewer than
-             * kidx_max/2 - 1 splitters rank before it in the order (more
-             * picks first, then smaller index). */
-            int w = 0;
-            for (int i = 0; i < u; i++) {
-                int before = 0;
-                for (int j = 0; j < u; j++)
-                    if (picks[j] > picks[i] || (picks[j] == picks[i] && j < i)) before++;
-                if (before < keep_n) {
+        if (dup && need > kidx_max && kidx_max >= 4 && u > keep_n) {
+            /* DESIGN R10 (round 2, revised again): drop u - keep_n unique
+             * splitters, one at a time: the one with the fewest picks
+             * (smaller index first) among those whose neighbours in splitter
+             * order are both still kept -- so the open bucket that absorbs a
+             * dropped splitter's keys spans at most two former buckets.  If
+             * fewer can be dropped that way, k is halved (below). */
+            int drop_n = u - keep_n, got = 0;
+            char dropped[512];
+            memset(dropped, 0, sizeof dropped);
+            while (got < drop_n) {
+                int best = -1;
+                for (int i = 0; i < u; i++) {
+                    if (dropped[i] || (i > 0 && dropped[i - 1]) || (i + 1 < u && dropped[i + 1])) continue;
+                    if (best < 0 || picks[i] < picks[best]) best = i;
+                }
+                if (best < 0) break;
+                dropped[best] = 1;
+                got++;
+            }
+            if (got == drop_n) {
+                int w = 0;
+                for (int i = 0; i < u; i++) {
+                    if (dropped[i]) continue;
                     memmove(out + (size_t)w * D, out + (size_t)i * D, D);
                     w++;
                 }
+                u = w;
+                leaves = next_pow2_int(u + 1);
+                need = 2 * leaves;
             }
-            u = w;
-            leaves = next_pow2_int(u + 1);
-            need = 2 * leaves;
         }
         if (need <= kidx_max || k <= 2) {
             *equality = dup;

@@ -87,7 +87,8 @@ class StepInfo(ctypes.Structure):
 
 EXPORTS = ["ips4o_sort", "ips4o_sort_ex", "ips4o_sort_host", "ips4o_scratch_bytes",
            "ips4o_status_string", "ips4o_get_dtype_info", "ips4o_partition_step", "ips4o_classify",
-           "ips4o_device_status", "ips4o_release_memory"]
+           "ips4o_device_status", "ips4o_release_memory", "ips4o_sample", "ips4o_select_splitters",
+           "ips4o_partition_splitters"]
 
 _lib = None
 
@@ -121,6 +122,12 @@ def load(path: str = LIB_PATH):
     L.ips4o_device_status.restype = ci
     L.ips4o_release_memory.argtypes = [ci]
     L.ips4o_release_memory.restype = ci
+    L.ips4o_sample.argtypes = [vp, u64, ci, vp, u64, u64, vp]
+    L.ips4o_sample.restype = ci
+    L.ips4o_select_splitters.argtypes = [vp, u64, ci, vp, ci, vp]
+    L.ips4o_select_splitters.restype = ci
+    L.ips4o_partition_splitters.argtypes = [vp, u64, ci, vp, vp, ci, ctypes.POINTER(ctypes.c_uint64)]
+    L.ips4o_partition_splitters.restype = ci
     _lib = L
     return L
 
@@ -257,3 +264,38 @@ def classify(elems, dtype: int, splitters_raw: bytes, u: int, equality: bool, ou
     _check(load().ips4o_classify(ptr, n, dtype, ctypes.cast(buf, ctypes.c_void_p), u, int(equality),
                                  out.data_ptr(), stream))
     return out
+
+
+# ---------------------------------------------------------------- distributed samplesort steps
+def sample(t, dtype: int, m: int, seed: int, out) -> None:
+    """ips4o_sample: m samples (DESIGN R8 draw, `seed`) of CUDA tensor t into
+    CUDA tensor out (m elements), stream-ordered."""
+    ptr, n, stream = _tensor_args(t, dtype)
+    optr, on, _ = _tensor_args(out, dtype)
+    if on < m:
+        raise IPS4OError("out holds fewer than m elements")
+    _check(load().ips4o_sample(ptr, n, dtype, stream, m, seed, optr))
+
+
+def select_splitters(samples, dtype: int, parts: int, out) -> None:
+    """ips4o_select_splitters: sort CUDA tensor `samples` in place and write the
+    parts-1 equidistant picks into CUDA tensor out, stream-ordered."""
+    ptr, n, stream = _tensor_args(samples, dtype)
+    optr, on, _ = _tensor_args(out, dtype)
+    if on < parts - 1:
+        raise IPS4OError("out holds fewer than parts - 1 elements")
+    _check(load().ips4o_select_splitters(ptr, n, dtype, stream, parts, optr))
+
+
+def partition_splitters(t, dtype: int, splitters, nspl: int) -> list:
+    """ips4o_partition_splitters: partition CUDA tensor t in place into nspl+1
+    ranges by the nspl sorted splitters (CUDA tensor); returns the nspl+2
+    range bounds (synchronous)."""
+    ptr, n, stream = _tensor_args(t, dtype)
+    sptr, sn, _ = _tensor_args(splitters, dtype)
+    if sn < nspl:
+        raise IPS4OError("splitters holds fewer than nspl elements")
+    b = (ctypes.c_uint64 * (nspl + 2))()
+    _check(load().ips4o_partition_splitters(ptr, n, dtype, stream, sptr, nspl, b))
+    return [int(x) for x in b]
+

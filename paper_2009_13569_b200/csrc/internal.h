@@ -128,6 +128,10 @@ struct LevelArgs {
   const u32 *measure_part;    // [2 * nmeasure_parts]: task, part | nparts << 16 (K0m)
   const u32 *measure_task;    // [3 * nmeasure]: task, first part, nparts (K0m)
   void *measure_out;          // [nmeasure_parts] PrepassPart: per-part key min/max
+  const char *ext_spl;        // round 0 of ips4o_partition_splitters: the given splitters
+                              // (ext_n elements, sorted) replace the sample's picks
+  u32 ext_n;
+  u32 pad_ext;
 };
 
 // The packed per-bucket permutation word: high 32

@@ -185,6 +185,8 @@ struct Call {
   int max_levels = 0;
   u64 arena_bytes = 0;
   bool skip_prepass = false, skip_basecase = false, timing = false, capture = false;
+  const char *ext_spl = nullptr;  // ips4o_partition_splitters: the given splitters (device)
+  int ext_n = 0;
 };
 
 static int parse_options(Call &k, const ips4o_options *opt) {
@@ -229,6 +231,8 @@ template <int DT> static SortCfg make_cfg(const Call &k, const DevState &ds, cha
   c.skip_basecase = k.skip_basecase;
   c.timing = k.timing;
   c.capture = k.capture;
+  c.ext_spl = k.ext_spl;
+  c.ext_n = k.ext_n;
   c.dbg_one_agent = env_int("IPS4O_DEBUG_ONE_AGENT", 0, 0, 1);
   // profiling mode: every round launched from the host (one synchronisation
   // per round) so that ncu sees each kernel; same plans, grids and kernels
@@ -561,15 +565,28 @@ static int dtype_align(int dtype) {
   }
 }
 
+// Development builds may compile one element type only (-DIPS4O_ONLY_DT=<dt>,
+// a quicker build for kernel experiments; the other types then return
+// IPS4O_ERR_INVALID).  Release builds compile all of them.
+template <int DT>
+static int run_dt(const Call &k, char *base, u64 n, cudaStream_t st, SortCtl *hctl, u64 *scratch,
+                  ips4o_step_info *cap) {
+#ifdef IPS4O_ONLY_DT
+  if constexpr (DT != IPS4O_ONLY_DT) return IPS4O_ERR_INVALID;
+  else
+#endif
+    return Sorter<DT>::run(k, base, n, st, hctl, scratch, cap);
+}
+
 static int dispatch(int dtype, const Call &k, char *base, u64 n, cudaStream_t st, SortCtl *hctl, u64 *scratch,
                     ips4o_step_info *cap) {
   switch (dtype) {
-    case DT_U64: return Sorter<DT_U64>::run(k, base, n, st, hctl, scratch, cap);
-    case DT_F64: return Sorter<DT_F64>::run(k, base, n, st, hctl, scratch, cap);
-    case DT_PAIR: return Sorter<DT_PAIR>::run(k, base, n, st, hctl, scratch, cap);
-    case DT_REC100: return Sorter<DT_REC100>::run(k, base, n, st, hctl, scratch, cap);
-    case DT_U32: return Sorter<DT_U32>::run(k, base, n, st, hctl, scratch, cap);
-    case DT_QUARTET: return Sorter<DT_QUARTET>::run(k, base, n, st, hctl, scratch, cap);
+    case DT_U64: return run_dt<DT_U64>(k, base, n, st, hctl, scratch, cap);
+    case DT_F64: return run_dt<DT_F64>(k, base, n, st, hctl, scratch, cap);
+    case DT_PAIR: return run_dt<DT_PAIR>(k, base, n, st, hctl, scratch, cap);
+    case DT_REC100: return run_dt<DT_REC100>(k, base, n, st, hctl, scratch, cap);
+    case DT_U32: return run_dt<DT_U32>(k, base, n, st, hctl, scratch, cap);
+    case DT_QUARTET: return run_dt<DT_QUARTET>(k, base, n, st, hctl, scratch, cap);
     default: return IPS4O_ERR_INVALID;
   }
 }
@@ -787,6 +804,125 @@ int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream, const i
                   reinterpret_cast<SortCtl *>(hbuf.data()), nullptr, info);
 }
 
+// ---------------------------------------------------------------- distributed samplesort
+int ips4o_sample(const void *ptr, uint64_t n, int dtype, void *stream, uint64_t m, uint64_t seed, void *out) {
+  const int D = dtype_bytes(dtype);
+  if (!D) return IPS4O_ERR_INVALID;
+  if (m == 0) return IPS4O_OK;
+  if (n == 0 || !ptr || !out || ((uintptr_t)ptr % 4) || ((uintptr_t)out % 4) || m >= (1ull << 40))
+    return IPS4O_ERR_INVALID;
+  DevState *ds = nullptr;
+  int rc = device_state(ds);
+  if (rc) return rc;
+  const u64 words = m * (u64)(D / 4);
+  const u64 grid = std::min<u64>((words + 255) / 256, (u64)ds->sms * 8);
+  gather_sample_kernel<<<(unsigned)grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const char *>(ptr), n, seed, m, D, reinterpret_cast<char *>(out));
+  CK(cudaGetLastError());
+  return IPS4O_OK;
+}
+
+int ips4o_select_splitters(void *samples, uint64_t total, int dtype, void *stream, int parts, void *out) {
+  const int D = dtype_bytes(dtype);
+  if (!D || parts < 1) return IPS4O_ERR_INVALID;
+  if (parts == 1) return IPS4O_OK;
+  if (!samples || !out || total < (uint64_t)parts || ((uintptr_t)out % 4)) return IPS4O_ERR_INVALID;
+  int rc = ips4o_sort(samples, total, dtype, stream);
+  if (rc) return rc;
+  const int words = (parts - 1) * (D / 4);
+  pick_kernel<<<(words + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const char *>(samples), total, parts, D, reinterpret_cast<char *>(out));
+  CK(cudaGetLastError());
+  return IPS4O_OK;
+}
+
+}  // extern "C"
+
+namespace ips4o {
+// order of the keys of two elements (host; the dtype's comparator, Alg. 3/4)
+template <int DT> static int cmp_elem_keys(const unsigned char *a, const unsigned char *b) {
+  u64 x[KEY_WORDS] = {0}, y[KEY_WORDS] = {0};
+  raw_to_key<DT>(a, x);
+  raw_to_key<DT>(b, y);
+  for (int i = KEY_WORDS - 1; i >= 0; --i)
+    if (x[i] != y[i]) return x[i] < y[i] ? -1 : 1;
+  return 0;
+}
+
+template <int DT>
+static int partition_splitters_impl(char *ptr, u64 n, cudaStream_t st, const char *splitters, int nspl,
+                                    uint64_t *bounds) {
+  constexpr int D = Traits<DT>::D, KI = Traits<DT>::KIDX;
+  if (nspl > KI / 2 - 1) return IPS4O_ERR_INVALID;
+  std::vector<unsigned char> hs((size_t)nspl * D), he(D);
+  CK(cudaMemcpyAsync(hs.data(), splitters, hs.size(), cudaMemcpyDeviceToHost, st));
+  if (n == 1) CK(cudaMemcpyAsync(he.data(), ptr, D, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto S = [&](int r) { return hs.data() + (size_t)r * D; };
+  for (int r = 1; r < nspl; ++r)
+    if (cmp_elem_keys<DT>(S(r - 1), S(r)) > 0) return IPS4O_ERR_INVALID;  // not sorted
+  bounds[0] = 0;
+  bounds[nspl + 1] = n;
+  if (n < 2) {  // nothing to partition: count the element (if any) per range
+    for (int r = 0; r < nspl; ++r) bounds[r + 1] = (n == 1 && cmp_elem_keys<DT>(he.data(), S(r)) <= 0) ? 1 : 0;
+    return IPS4O_OK;
+  }
+  Call k;
+  k.capture = true;
+  k.ext_spl = splitters;
+  k.ext_n = nspl;
+  std::vector<char> hbuf(CTL_READ);
+  std::vector<uint64_t> E(KI + 1);
+  std::vector<unsigned char> tr((size_t)KI * 24), sp((size_t)KI * 24);
+  ips4o_step_info info;
+  memset(&info, 0, sizeof info);
+  info.E = E.data();
+  info.tree = tr.data();
+  info.splitter = sp.data();
+  int rc = Sorter<DT>::run(k, ptr, n, st, reinterpret_cast<SortCtl *>(hbuf.data()), nullptr, &info);
+  if (rc) return rc;
+  // range r = (S_{r-1}, S_r]: the elements <= S_r are the buckets up to the
+  // one of S_r's unique index u (u + 1 buckets, or 2u + 2 with equality
+  // buckets: (s_{u-1}, s_u) and {s_u} per unique splitter)
+  int u = -1;
+  for (int r = 0; r < nspl; ++r) {
+    if (r == 0 || cmp_elem_keys<DT>(S(r - 1), S(r)) != 0) ++u;
+    const int nb = info.equality ? 2 * u + 2 : u + 1;
+    if (nb > info.num_buckets) {
+      g_err = "partition_splitters: bucket layout does not match the splitters";
+      return IPS4O_ERR_CUDA;
+    }
+    bounds[r + 1] = E[nb];
+  }
+  return IPS4O_OK;
+}
+}  // namespace ips4o
+
+extern "C" {
+int ips4o_partition_splitters(void *ptr, uint64_t n, int dtype, void *stream, const void *splitters, int nspl,
+                              uint64_t *bounds) {
+  const int D = dtype_bytes(dtype);
+  if (!D || !bounds || nspl < 1 || !splitters || ((uintptr_t)splitters % 4)) return IPS4O_ERR_INVALID;
+  if (n > 0 && (!ptr || ((uintptr_t)ptr % dtype_align(dtype)) || n >= (1ull << 32))) return IPS4O_ERR_INVALID;
+  char *p = reinterpret_cast<char *>(ptr);
+  const char *s = reinterpret_cast<const char *>(splitters);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (dtype) {
+#ifdef IPS4O_ONLY_DT
+#define PS(DTc) return DTc == IPS4O_ONLY_DT ? partition_splitters_impl<DTc == IPS4O_ONLY_DT ? DTc : IPS4O_ONLY_DT>(p, n, st, s, nspl, bounds) : IPS4O_ERR_INVALID;
+#else
+#define PS(DTc) return partition_splitters_impl<DTc>(p, n, st, s, nspl, bounds);
+#endif
+    case DT_U64: PS(DT_U64)
+    case DT_F64: PS(DT_F64)
+    case DT_PAIR: PS(DT_PAIR)
+    case DT_REC100: PS(DT_REC100)
+    case DT_U32: PS(DT_U32)
+    case DT_QUARTET: PS(DT_QUARTET)
+#undef PS
+    default: return IPS4O_ERR_INVALID;
+  }
+}
 }  // extern "C"
 
 namespace ips4o {

@@ -488,8 +488,26 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       }
     }
     if (cnt == T) {
+      // a warp whose 32 elements share one bucket (presorted or
+      // duplicate-heavy runs: RootDup, AlmostSorted) takes its ranks with one
+      // atomic instead of 32 same-address ones (tested on the first element
+      // of the thread; the other elements of such a tile are tested too)
+      if (__all_sync(0xffffffffu, bkt[0] == __shfl_sync(0xffffffffu, bkt[0], 0))) {
 #pragma unroll
-      for (int k = 0; k < IPT; ++k) rank[k] = atomicAdd(&s_tcnt[bkt[k]], 1u);
+        for (int k = 0; k < IPT; ++k) {
+          const u32 b0 = __shfl_sync(0xffffffffu, bkt[k], 0);
+          if (__all_sync(0xffffffffu, bkt[k] == b0)) {
+            u32 r0 = 0;
+            if (lane == 0) r0 = atomicAdd(&s_tcnt[b0], 32u);
+            rank[k] = __shfl_sync(0xffffffffu, r0, 0) + (u32)lane;
+          } else {
+            rank[k] = atomicAdd(&s_tcnt[bkt[k]], 1u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) rank[k] = atomicAdd(&s_tcnt[bkt[k]], 1u);
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < IPT; ++k) rank[k] = (tid + k * NT < cnt) ? atomicAdd(&s_tcnt[bkt[k]], 1u) : 0u;

@@ -350,4 +350,28 @@ __global__ void measure_reduce_kernel(LevelArgs A, u32 nmeasure) {
   key_to_words<Key>(mx, t.hi);
 }
 
+// ---------------------------------------------------------------- distributed samplesort
+// The sample of one shard: element j is A[sample_index(seed, 0, 0, n, j)]
+// (the counter-based draw of DESIGN R8, "task" = the whole shard), copied as
+// D bytes (D is a multiple of 4).
+__global__ void gather_sample_kernel(const char *base, u64 n, u64 seed, u64 m, int D, char *out) {
+  const int w = D / 4;
+  for (u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x; x < m * (u64)w; x += (u64)gridDim.x * blockDim.x) {
+    const u64 j = x / (u64)w, q = x % (u64)w;
+    const u64 i = sample_index(seed, 0, 0, n, j);
+    reinterpret_cast<u32 *>(out)[j * w + q] = reinterpret_cast<const u32 *>(base + i * (u64)D)[q];
+  }
+}
+
+// Splitter j < parts - 1 of the sorted global sample: the element at rank
+// ((j + 1) * total) / parts - 1 (equidistant picks).
+__global__ void pick_kernel(const char *sorted, u64 total, int parts, int D, char *out) {
+  const int w = D / 4;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < (parts - 1) * w; x += gridDim.x * blockDim.x) {
+    const int j = x / w, q = x % w;
+    const u64 r = ((u64)(j + 1) * total) / (u64)parts - 1;
+    reinterpret_cast<u32 *>(out)[(u64)j * w + q] = reinterpret_cast<const u32 *>(sorted + r * (u64)D)[q];
+  }
+}
+
 }  // namespace ips4o

@@ -53,6 +53,8 @@ struct SortCfg {
   u64 list_cap;        // tasks per pending list
   u64 arena_off, arena_cap;
   u32 *status;         // persistent per-device status word (ips4o_device_status)
+  const char *ext_spl; // ips4o_partition_splitters: given splitters (device, ext_n elements)
+  int ext_n;
 };
 
 // Device-side state of one sort (at the start of the scratch).
@@ -104,6 +106,7 @@ template <int DT> __host__ __device__ TaskShape task_shape(const SortCfg &c, u64
   u64 kr = npow2(cdiv(2 * size, M > 0 ? M : 1));
   kr = kr < 2 ? 2 : kr;
   kr = kr > (u64)c.k_max ? (u64)c.k_max : kr;
+  if (c.ext_n > 0) kr = (u64)c.k_max;  // given splitters: every bucket index available
   s.kr = (u32)kr;
   const u64 kx = c.algo == ALGO_TREE ? 2 * kr : kr;
   s.kidx = (u32)(kx < (u64)KI ? kx : (u64)KI);
@@ -246,6 +249,8 @@ __host__ __device__ LevelArgs level_args(SortCtl *ctl, const SortCfg &c, const P
   A.go = r == 0 ? &ctl->go : nullptr;
   A.nmparts = (u32)tot.mparts;
   A.nmtasks = (u32)tot.mtasks;
+  A.ext_spl = r == 0 ? c.ext_spl : nullptr;
+  A.ext_n = r == 0 ? (u32)c.ext_n : 0u;
   u32 stg = 0;
   if (ALGO == ALGO_DIGIT && tot.mtasks > 0) stg |= (1u << ST_MEAS) | (1u << ST_MEASRED);
   for (int x = ST_SAMPLE; x <= ST_CFILL; ++x) stg |= 1u << x;

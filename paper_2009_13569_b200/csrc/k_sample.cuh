@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   const unsigned short *s_end = reinterpret_cast<const unsigned short *>(s_hist);
   __shared__ Key s_cand[256], s_pick[256], s_red[2][32];
   __shared__ int s_wt[256];  // picks per unique splitter (R10)
+  __shared__ unsigned char s_drop[256];
   __shared__ u32 s_ws[SAMPLE_THREADS / 32 + 1];
   __shared__ int s_u, s_leaves, s_k, s_slow;
   Key *tree = reinterpret_cast<Key *>(A.trees) + (size_t)ti * 2 * Tr::KIDX;
@@ -224,7 +225,10 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   static_assert((1 << DB) >= sample_max<DT>(), "one digit per sample");
   constexpr int RUNMAX = 32;                       // longer runs: full sort instead
 
-  const int m = (int)L.m;
+  // ips4o_partition_splitters: the picks are the given (sorted) splitters and
+  // nothing is sampled (the distributed samplesort)
+  const bool ext = A.ext_n > 0;
+  const int m = ext ? 0 : (int)L.m;
   const int P = next_pow2_i(m) > SORT_THREADS ? next_pow2_i(m) : SORT_THREADS;
   // P:726 "we sample k*alpha elements" (gathered, not swapped: DESIGN R9);
   // all of a thread's sample loads are issued before any is used
@@ -263,6 +267,10 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   for (int w = 1; w < NT / 32; ++w) {
     kmin = s_red[0][w] < kmin ? s_red[0][w] : kmin;
     kmax = s_red[1][w] > kmax ? s_red[1][w] : kmax;
+  }
+  if (ext) {
+    kmin = Tr::key(A.ext_spl);
+    kmax = Tr::key(A.ext_spl + (size_t)(A.ext_n - 1) * Tr::D);
   }
   int lg = 1;
   while ((1 << lg) < m && lg < DB) ++lg;
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   if (tid == 0) {
     key_to_words<Key>(kmin, L.lut_lo);
     key_to_words<Key>(kmax, L.lut_hi);
-    s_k = (int)L.k_req;
+    s_k = ext ? (int)A.ext_n + 1 : (int)L.k_req;
   }
   // P:728 equidistant picks; P:729 dedupe; P:733 equality buckets iff a
   // duplicate was removed (R23); R10: keep the most-picked equality
@@ -352,7 +360,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
     const int alpha = m / k;
     if (tid < k - 1) {
       const int p = (tid + 1) * alpha - 1;
-      s_pick[tid] = all_equal ? kmin : sorted ? s_keys[p] : pick(p);
+      s_pick[tid] = ext ? Tr::key(A.ext_spl + (size_t)tid * Tr::D) : all_equal ? kmin : sorted ? s_keys[p] : pick(p);
     }
     __syncthreads();
     if (s_slow && !sorted) {
@@ -388,34 +396,38 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
       int leaves = next_pow2_i(u + 1);
       int need = dup ? 2 * leaves : leaves;
       const int up = (int)L.kidx / 2 - 1;
-      if (dup && need > (int)L.kidx && L.kidx >= 4 && u - up <= (up / 8 > 1 ? up / 8 : 1)) {
-        // R10: the bucket indices of u equality splitters exceed the budget by
-        // a few splitters: keep the kidx/2 - 1 picked most often (the
-        // heaviest keys keep their equality buckets), ties by rank; k is
-        // unchanged.  (More to drop: halve k below, which keeps the
-        // splitters evenly spread.)
-        auto at_least = [&](int w) {
-          int c = 0;
-          for (int i = 0; i < u; ++i) c += s_wt[i] >= w ? 1 : 0;
-          return c;
-        };
-        int lo = 1, hi = k;  // largest T with #{wt >= T} >= up
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (at_least(mid) >= up) lo = mid;
-          else hi = mid - 1;
+      if (dup && need > (int)L.kidx && L.kidx >= 4 && u > up) {
+        // R10: u - up unique splitters too many for the bucket indices: drop
+        // them one at a time, fewest picks first (ties: the smaller), never
+        // two neighbours (the open bucket that absorbs a dropped splitter's
+        // keys then spans at most two former buckets; RootDup's level 2 keeps
+        // every bucket at one key value).  Passes over the pick counts in
+        // increasing order; each pass scans the splitters in order, which is
+        // the same sequence of choices.  k is unchanged; if fewer can be
+        // dropped, k is halved below (the splitters stay evenly spread).
+        const int want = u - up;
+        int got = 0, wprev = 0;
+        for (int i = 0; i < u; ++i) s_drop[i] = 0;
+        while (got < want) {
+          int wc = 0x7fffffff;
+          for (int i = 0; i < u; ++i)
+            if (!s_drop[i] && s_wt[i] > wprev && s_wt[i] < wc) wc = s_wt[i];
+          if (wc == 0x7fffffff) break;
+          for (int i = 0; i < u && got < want; ++i)
+            if (s_wt[i] == wc && !s_drop[i] && !(i > 0 && s_drop[i - 1]) && !(i + 1 < u && s_drop[i + 1])) {
+              s_drop[i] = 1;
+              ++got;
+            }
+          wprev = wc;
         }
-        const int T = lo;
-        int take = up - at_least(T + 1);
-        int w = 0;
-        for (int i = 0; i < u; ++i) {
-          const bool keep = s_wt[i] > T || (s_wt[i] == T && take > 0);
-          if (s_wt[i] == T && keep) --take;
-          if (keep) s_cand[w++] = s_cand[i];
+        if (got == want) {
+          int w = 0;
+          for (int i = 0; i < u; ++i)
+            if (!s_drop[i]) s_cand[w++] = s_cand[i];
+          u = w;
+          leaves = next_pow2_i(u + 1);
+          need = 2 * leaves;
         }
-        u = w;
-        leaves = next_pow2_i(u + 1);
-        need = 2 * leaves;
       }
       if (need <= (int)L.kidx || k <= 2) {
         L.K = (u32)need;

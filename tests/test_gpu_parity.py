@@ -171,6 +171,36 @@ def test_partition_step_tree(ips, orc, dtype, n, kind):
         assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1, j
 
 
+@pytest.mark.parametrize("nvals,shuffle", [(140, False), (200, True), (131, True), (250, False)])
+def test_partition_step_equality_budget(ips, orc, nvals, shuffle):
+    """R10 (DESIGN): more unique equality splitters than bucket indices.  With
+    nvals heavy key values every value is picked; 140, 131 and 200 values are
+    thinned (never two neighbours dropped); 250 cannot be thinned enough.  The tree must equal
+    the oracle's; every bucket holds exactly its oracle-sorted range."""
+    n = 1 << 21
+    a = (np.arange(n, dtype=np.uint64) % np.uint64(nvals)) * np.uint64(7919)
+    if shuffle:
+        a = np.random.default_rng(nvals).permutation(a)
+    t = to_dev(a)
+    info = ips.partition_step(t, U64, base_cap=2048)
+    g = from_dev(t, a)
+    st = orc.sample_tree(a, U64, 0, n, info["seed"], 0, info["k_req"],
+                         info["samples"] // info["k_req"], info["kidx_budget"])
+    assert st["l"] == info["l"] and st["equality"] == info["equality"] and st["k"] == info["k_used"]
+    assert np.array_equal(info["splitter"], key_bytes_of(st["splitter"], U64).reshape(-1))
+    E = info["E"]
+    o = orc.sort(a, U64)
+    for j in range(info["num_buckets"]):
+        e0, e1 = int(E[j]), int(E[j + 1])
+        assert np.array_equal(np.sort(g[e0:e1]), o[e0:e1]), j
+    if nvals < 250:
+        # thinned, not halved: an open bucket holds a dropped splitter's keys
+        # and at most one unpicked value (140 and 131: none)
+        assert info["equality"] and info["k_used"] == info["k_req"]
+        vmax = 1 if nvals < 200 else 2
+        assert np.diff(E.astype(np.int64)).max() <= vmax * (n // nvals + 1)
+
+
 @pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("n", [5003, 300007])
 def test_partition_step_digit(ips, orc, dtype, n):

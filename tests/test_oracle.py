@@ -385,24 +385,31 @@ def test_classifier_f64_and_rec100_use_the_dtype_order(orc):
 
 
 def test_select_splitters_equality_budget(orc):
-    """R10: 255 picks from a sample with 200 zeros give 1 + 205 unique
-    splitters; 2*256 indices do not fit 256 and 79 are too many to thin away
-    (more than 127/8), so the pick is repeated with k/2 (127 candidates).  With
-    128 unique splitters (1 over the budget) the 127 picked most often stay:
-    the heaviest keys keep their equality buckets, ties keep the smaller."""
+    """R10 (DESIGN): with equality buckets the u unique splitters must leave
+    2*(u+1) <= kidx_max bucket indices.  The u - (kidx_max/2 - 1) surplus
+    splitters are dropped one at a time, fewest picks first (ties: the
+    smaller), never two neighbours; if that many cannot be dropped, k is
+    halved.  Expected splitters are worked out by hand in the comments."""
     m = 256 * 4
+    # 200 zeros, then 1..824: picks at 4j+3 give 0 (50 times) and 4i for
+    # i = 1..205 (once each): u = 206, 79 too many -> drop i = 1, 3, .., 157
     sample = np.sort(np.concatenate([np.zeros(200, dtype=np.uint64),
                                      np.arange(1, m - 199, dtype=np.uint64)]))
     sp, eq, kf = orc.select_splitters(sample, 256, 256, U64)
-    assert kf == 128 and eq
-    u = sp.size // 8
-    leaves = 1 << math.ceil(math.log2(u + 1))
-    assert 2 * leaves <= 256
-    # 128 unique picks (one over the budget): 0 picked 128 times, 1..127 once each
+    want = [0] + [4 * i for i in range(2, 159, 2)] + [4 * i for i in range(159, 206)]
+    assert kf == 256 and eq and sp.view(np.uint64).tolist() == want
+    # 128 unique picks (one over the budget): 0 picked 128 times, 1..127 once
+    # each -> the first of the lightest, 1, is dropped
     s2 = np.sort(np.concatenate([np.zeros(512, dtype=np.uint64), np.repeat(np.arange(1, 129, dtype=np.uint64), 4)]))
     sp3, eq3, kf3 = orc.select_splitters(s2, 256, 256, U64)
     got = sp3.view(np.uint64).tolist()
-    assert eq3 and kf3 == 256 and got == list(range(0, 127)), got
+    assert eq3 and kf3 == 256 and got == [0] + list(range(2, 128)), got
+    # budget 64 (31 equality splitters): k = 256 has u = 206 (at most 103
+    # droppable), k = 128 has u = 103 (51 droppable, 72 needed); k = 64 picks
+    # 0 (12 times) and 16i - 8 for i = 1..51: drop i = 1, 3, .., 41
+    sp4, eq4, kf4 = orc.select_splitters(sample, 256, 64, U64)
+    want4 = [0] + [16 * i - 8 for i in range(2, 43, 2)] + [16 * i - 8 for i in range(43, 52)]
+    assert kf4 == 64 and eq4 and sp4.view(np.uint64).tolist() == want4, sp4.view(np.uint64).tolist()
     sp2, eq2, kf2 = orc.select_splitters(np.arange(m, dtype=np.uint64), 256, 256, U64)
     assert kf2 == 256 and not eq2 and sp2.size // 8 == 255
 
