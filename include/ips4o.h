@@ -267,6 +267,10 @@ typedef struct ips4o_step_info {
     uint64_t *E;           /* [num_buckets + 1] exact bucket boundaries (out)     */
     void *tree;            /* [2^l] keys (out, TREE)                              */
     void *splitter;        /* [2^l] keys (out, TREE)                              */
+    int32_t lut_log;       /* lookup table of starting leaves (TREE, keys <= 16 B):
+                              0 = linear slots, M > 0 = logarithmic slots with M
+                              mantissa bits (DESIGN "Classification")          */
+    int32_t reserved0;
 } ips4o_step_info;
 int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream,
                          const ips4o_options *opt, ips4o_step_info *info);

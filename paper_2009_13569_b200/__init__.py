@@ -82,6 +82,7 @@ class StepInfo(ctypes.Structure):
         ("samples", ctypes.c_int32), ("kidx_budget", ctypes.c_int32), ("level", ctypes.c_int32),
         ("seed", ctypes.c_uint64),
         ("E", ctypes.POINTER(ctypes.c_uint64)), ("tree", ctypes.c_void_p), ("splitter", ctypes.c_void_p),
+        ("lut_log", ctypes.c_int32), ("reserved0", ctypes.c_int32),
     ]
 
 
@@ -252,7 +253,7 @@ def partition_step(t, dtype: int, **opts) -> dict:
         "E": np.array(E[: K + 1], dtype=np.uint64),
         "tree": np.frombuffer(bytes(tree), dtype=np.uint8)[: leaves * kb].copy(),
         "splitter": np.frombuffer(bytes(spl), dtype=np.uint8)[: leaves * kb].copy(),
-        "key_bytes": kb,
+        "key_bytes": kb, "lut_log": info.lut_log,
     }
 
 

@@ -243,6 +243,27 @@ constexpr int LUT_BITS = 14;
 constexpr u32 LUT_SLOTS = 1u << LUT_BITS;
 constexpr u32 LUT_FIN = 1u << 15;
 
+// Slot of a key offset d = x - llo in a lookup table.  Linear (logm = 0):
+// d >> ls.  Logarithmic (logm = M > 0): exact below 2^M, then 2^M slots per
+// octave -- d in [2^e, 2^(e+1)) (e >= M) maps to 2^M (e - M) + (d >> (e - M)),
+// monotone and contiguous (relative resolution 2^-M): dense at the low end of
+// the range, for distributions whose splitters crowd there (Zipf).  The
+// caller clamps to the table's last used slot.
+__device__ __forceinline__ u32 lut_slot_of(u64 d, int ls, int logm) {
+  if (logm == 0) return (u32)min(d >> ls, (u64)0xFFFFFFFFu);
+  if (d < (2ull << logm)) return (u32)d;
+  const int e = 63 - __clzll((long long)d);
+  return (u32)(((u64)(e - logm) << logm) + (d >> (e - logm)));
+}
+// First offset of slot q (inverse of lut_slot_of on slot starts).
+__device__ __forceinline__ u64 lut_slot_start(u32 q, int ls, int logm) {
+  if (logm == 0) return (u64)q << ls;
+  if (q < (2u << logm)) return q;
+  const u32 j = q >> logm;  // >= 2: e = j + logm - 1
+  const u64 t = (u64)q - ((u64)(j - 1) << logm);
+  return t << (j - 1);
+}
+
 // ------------------------------------------------------------------ RNG (DESIGN R8)
 constexpr u64 GAMMA = 0x9E3779B97F4A7C15ull;
 __host__ __device__ __forceinline__ u64 mix64(u64 z) {

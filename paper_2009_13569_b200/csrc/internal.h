@@ -61,7 +61,7 @@ struct LevelTask {
   u32 equality;      // equality buckets on (TREE)
   int shift;         // digit shift (DIGIT)
   u32 k_used;        // k after the equality-budget rule (DESIGN R10)
-  u32 pad1;
+  u32 lut_log;       // lookup-table slot mapping: 0 linear, M > 0 logarithmic (lut_slot_of)
   u64 lut_lo[KEY_WORDS];  // key range of the sample (TREE); after K1: the first key of
   u64 lut_hi[KEY_WORDS];  // the lookup table's slot 1 grid (llo) and the sample maximum
   u32 lut_ls;             // lookup table (K1 builds it once per task): slot of key x =
@@ -128,6 +128,14 @@ struct LevelArgs {
   const u32 *measure_part;    // [2 * nmeasure_parts]: task, part | nparts << 16 (K0m)
   const u32 *measure_task;    // [3 * nmeasure]: task, first part, nparts (K0m)
   void *measure_out;          // [nmeasure_parts] PrepassPart: per-part key min/max
+  // count-first finish of narrow-range key-only tasks (k_count.cuh; K6 appends)
+  TaskDesc *count_tasks;      // [count_cap] tasks (counters[9] appended this round)
+  u32 *count_off;             // [count_cap] offset of the task's counters in count_hist
+  u32 *count_hist;            // [CNT_POOL] per-value counts (counters[10] reserved)
+  u32 *count_pre;             // [count_cap + 1] exclusive prefix of the tasks' chunk counts
+  u32 *count_work;            // [2] work counters of K9b, K9c
+  u32 count_cap;
+  u32 count_grid;             // persistent CTAs of K9b / K9c
   const char *ext_spl;        // round 0 of ips4o_partition_splitters: the given splitters
                               // (ext_n elements, sorted) replace the sample's picks
   u32 ext_n;
@@ -159,13 +167,13 @@ enum : u32 {
 // start, [slot][1] = latest warp end.  Host folds them into kernel families.
 enum KSlot {
   KS_PRESAMPLE = 0, KS_PREPASS, KS_PREREDUCE, KS_MEASURE, KS_MEASURE_RED, KS_SAMPLE, KS_CLASSIFY,
-  KS_BOUND, KS_FIX, KS_PERM, KS_CSAVE, KS_CFILL, KS_BASE, KS_SPLIT, KS_REV, KS_PLAN, KS_COUNT
+  KS_BOUND, KS_FIX, KS_PERM, KS_CSAVE, KS_CFILL, KS_BASE, KS_SPLIT, KS_REV, KS_PLAN, KS_NARROW, KS_COUNT
 };
 
 // The kernels of one round, in launch order (k_plan.cuh launch_stage).
 enum Stage {
-  ST_MEAS = 0, ST_MEASRED, ST_SAMPLE, ST_CLASSIFY, ST_BOUND, ST_FIX, ST_PERM, ST_CSAVE, ST_CFILL, ST_BASE,
-  ST_SPLIT, ST_NEXT, ST_N
+  ST_MEAS = 0, ST_MEASRED, ST_SAMPLE, ST_CLASSIFY, ST_BOUND, ST_FIX, ST_PERM, ST_CSAVE, ST_CFILL, ST_CSETUP,
+  ST_CCOUNT, ST_CWRITE, ST_BASE, ST_SPLIT, ST_NEXT, ST_N
 };
 
 struct PrepassOut {

@@ -53,7 +53,7 @@ static int set_cuda_err(cudaError_t e, const char *what, int line) {
 enum KFam { KF_PRE = 0, KF_SAMPLE, KF_CLASSIFY, KF_BOUND, KF_FIX, KF_PERM, KF_CLEAN, KF_SCHED, KF_BASE, KF_REV, KF_PLAN, KF_TOTAL };
 static const int kSlotFamily[KS_COUNT] = {
     KF_PRE,  KF_PRE,  KF_PRE,   KF_SAMPLE, KF_SAMPLE, KF_SAMPLE, KF_CLASSIFY, KF_BOUND,
-    KF_FIX,  KF_PERM, KF_CLEAN, KF_CLEAN,  KF_BASE,   KF_BASE,   KF_REV,      KF_PLAN};
+    KF_FIX,  KF_PERM, KF_CLEAN, KF_CLEAN,  KF_BASE,   KF_BASE,   KF_REV,      KF_PLAN, KF_BASE};
 
 static const int NDT = 6;
 
@@ -298,7 +298,7 @@ static void fill_stats(const SortCtl &h, ips4o_stats *out, u64 scratch) {
     for (int k = 0; k < KS_COUNT; ++k) {
       const unsigned long long a = h.tslot[r][k][0], b = h.tslot[r][k][1];
       if (a == ~0ull || b < a) continue;
-      const int c = k == KS_CLASSIFY ? 0 : k == KS_PERM ? 1 : (k == KS_BASE || k == KS_SPLIT) ? 2 : 3;
+      const int c = k == KS_CLASSIFY ? 0 : k == KS_PERM ? 1 : (k == KS_BASE || k == KS_SPLIT || k == KS_NARROW) ? 2 : 3;
       out->round_kernel_ms[r][c] += (float)((double)(b - a) * 1e-6);
     }
   out->kernel_ms[KF_TOTAL] = t1 > t0 ? (float)((double)(t1 - t0) * 1e-6) : 0.f;
@@ -500,6 +500,13 @@ template <int DT> struct Sorter {
               A.base, A.split_tasks, ctl->counters + 8, A.base_cap_tasks, sp, A.tslot);
         break;
       }
+      case ST_CSETUP: count_setup_kernel<<<1, CNT_SETUP_THREADS, 0, st>>>(A); break;
+      case ST_CCOUNT:
+        if constexpr (BaseItem<DT>::KEY_ONLY) count_kernel<DT><<<A.count_grid, CNT_THREADS, 0, st>>>(A);
+        break;
+      case ST_CWRITE:
+        if constexpr (BaseItem<DT>::KEY_ONLY) count_write_kernel<DT><<<A.count_grid, CNT_THREADS, 0, st>>>(A);
+        break;
       case ST_NEXT: driver_kernel<DT, ALGO><<<1, PLAN_THREADS, 0, st>>>(ctl, 2); break;
       case ST_MEAS: measure_part_kernel<DT><<<A.nmparts, MEAS_THREADS, 0, st>>>(A); break;
       case ST_MEASRED: measure_reduce_kernel<DT><<<(A.nmtasks + 127) / 128, 128, 0, st>>>(A, A.nmtasks); break;
@@ -524,6 +531,7 @@ template <int DT> struct Sorter {
     info->kidx_budget = (int)L.kidx;
     info->level = 0;
     info->seed = h.cfg.seed;
+    info->lut_log = (int)L.lut_log;
     std::vector<u64> E(L.K + 1);
     CK(cudaMemcpy(E.data(), h.A.E + L.bucket_off, (L.K + 1) * 8, cudaMemcpyDeviceToHost));
     if (info->E) memcpy(info->E, E.data(), (L.K + 1) * 8);

@@ -388,6 +388,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   int ls = 0;
   u32 nlut_used = 1;
   bool span_task = false;
+  int lut_log = 0;
   const int nspl = (1 << l) - 1;
   constexpr u32 FIN = LUT_FIN;
   static_assert(KI <= 512, "bucket and splitter indices fit 9 bits");
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     ls = (int)L.lut_ls;
     nlut_used = L.lut_n;
     span_task = L.lut_span != 0;
+    lut_log = (int)L.lut_log;
     const uint4 *src = reinterpret_cast<const uint4 *>(A.luts + L.lut_off);
     for (u32 q = tid; q < (2u << L.lut_bits) / 16; q += NT) reinterpret_cast<uint4 *>(s_lut)[q] = src[q];
   }
@@ -443,18 +445,25 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       for (int k = 0; k < IPT; ++k) key[k] = elem_key<DT>(x[k]);
       if (ALGO == ALGO_TREE) {
         u32 ent[IPT];
+        if (lut_log) {
+          // logarithmic slots (lut_slot_of): keys below llo only outside span_task
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) {
-          const Key dk = key[k] - llo;
-          u32 q;
-          if (span_task) {
-            // keys lie in [tlo, thi]; the clamp only guards the unused lanes
-            // of a partial tile
-            q = min((u32)(dk >> ls), nlut_used - 1);
-          } else {
-            q = key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1);
+          for (int k = 0; k < IPT; ++k) {
+            const Key dk = key[k] - llo;
+            const u32 q = (!span_task && key[k] < llo) ? 0u : min(lut_slot_of((u64)dk, 0, lut_log), nlut_used - 1);
+            ent[k] = s_lut[q];
           }
-          ent[k] = s_lut[q];
+        } else if (span_task) {
+          // keys lie in [tlo, thi]; the clamp only guards the unused lanes of
+          // a partial tile
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) ent[k] = s_lut[min((u32)((key[k] - llo) >> ls), nlut_used - 1)];
+        } else {
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) {
+            const Key dk = key[k] - llo;
+            ent[k] = s_lut[key[k] < llo ? 0u : ((dk >> ls) < (Key)nlut_used ? (u32)(dk >> ls) : nlut_used - 1)];
+          }
         }
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {

@@ -2,6 +2,7 @@
 // (Alg. 2, adapted to device task lists).
 #pragma once
 #include "common.cuh"
+#include "k_count.cuh"
 #include "k_basecase.cuh"
 #include "k_classify.cuh"
 
@@ -210,6 +211,23 @@ __device__ void schedule_task(const LevelArgs &A, u32 ti, const u64 *sE) {
     // DIGIT: a digit that kept most of the task splits bits the keys do not
     // use (sparse keys); measure the child's exact range first (DESIGN R27)
     if (ALGO == ALGO_DIGIT && 2 * sz > L.t.size) c.flags |= TF_MEASURE;
+    if constexpr (BaseItem<DT>::KEY_ONLY) {
+      // a narrow key range larger than the base case: counted and written
+      // from the counts in this round (k_count.cuh, count-first)
+      if (sz > 65535 && sz > A.base_split_elems && A.count_cap && hi - lo < (Key)CNT_RANGE_MAX) {
+        const u32 R = (u32)(hi - lo) + 1;
+        const u32 off = atomicAdd(&A.counters[10], R);
+        if (off + R <= CNT_POOL) {
+          const u32 slot = atomicAdd(&A.counters[9], 1u);
+          if (slot < A.count_cap) {
+            A.count_tasks[slot] = c;
+            A.count_off[slot] = off;
+            atomicAdd(reinterpret_cast<unsigned long long *>(&A.counters[6]), (unsigned long long)sz);
+            continue;
+          }
+        }
+      }
+    }
     u32 *cnt;
     TaskDesc *list;
     u32 cap;

@@ -17,6 +17,7 @@
 #include "k_basecase.cuh"
 #include "k_classify.cuh"
 #include "k_cleanup.cuh"
+#include "k_count.cuh"
 #include "k_misc.cuh"
 #include "k_permute.cuh"
 #include "k_sample.cuh"
@@ -203,6 +204,14 @@ template <int DT> __host__ __device__ u64 layout(LevelArgs &A, char *base, const
   A.bc_scratch = BaseItem<DT>::SPLIT ? take(P.bc_grid * P.bc_cap * sizeof(typename BaseItem<DT>::Item)) : nullptr;
   A.base_tasks = reinterpret_cast<TaskDesc *>(take(P.child * sizeof(TaskDesc)));
   A.split_tasks = BaseItem<DT>::SPLIT ? reinterpret_cast<TaskDesc *>(take(P.child * sizeof(TaskDesc))) : nullptr;
+  if (BaseItem<DT>::KEY_ONLY) {  // count-first tasks (k_count.cuh): at most one per child
+    A.count_cap = (u32)P.child;
+    A.count_tasks = reinterpret_cast<TaskDesc *>(take(P.child * sizeof(TaskDesc)));
+    A.count_off = reinterpret_cast<u32 *>(take(P.child * 4));
+    A.count_pre = reinterpret_cast<u32 *>(take((P.child + 1) * 4));
+    A.count_work = reinterpret_cast<u32 *>(take(2 * 4));
+    A.count_hist = reinterpret_cast<u32 *>(take((u64)CNT_POOL * 4));
+  }
   return rup(used, 256);
 }
 
@@ -249,12 +258,15 @@ __host__ __device__ LevelArgs level_args(SortCtl *ctl, const SortCfg &c, const P
   A.go = r == 0 ? &ctl->go : nullptr;
   A.nmparts = (u32)tot.mparts;
   A.nmtasks = (u32)tot.mtasks;
+  A.count_grid = (u32)c.sms * 4;
+  if (c.capture || c.skip_basecase) A.count_cap = 0;  // (no count-first finish: K6 keeps such tasks)
   A.ext_spl = r == 0 ? c.ext_spl : nullptr;
   A.ext_n = r == 0 ? (u32)c.ext_n : 0u;
   u32 stg = 0;
   if (ALGO == ALGO_DIGIT && tot.mtasks > 0) stg |= (1u << ST_MEAS) | (1u << ST_MEASRED);
   for (int x = ST_SAMPLE; x <= ST_CFILL; ++x) stg |= 1u << x;
   if (!c.capture && !c.skip_basecase) {
+    if (BaseItem<DT>::KEY_ONLY) stg |= (1u << ST_CSETUP) | (1u << ST_CCOUNT) | (1u << ST_CWRITE);
     stg |= 1u << ST_BASE;
     if (BaseItem<DT>::SPLIT) stg |= 1u << ST_SPLIT;
   }
@@ -386,6 +398,13 @@ __device__ void launch_stage(const LevelArgs &A, int st, cudaStream_t tl) {
             A.base, A.split_tasks, ctl->counters + 8, A.base_cap_tasks, sp, A.tslot);
       break;
     }
+    case ST_CSETUP: count_setup_kernel<<<1, CNT_SETUP_THREADS, 0, tl>>>(A); break;
+    case ST_CCOUNT:
+      if constexpr (BaseItem<DT>::KEY_ONLY) count_kernel<DT><<<A.count_grid, CNT_THREADS, 0, tl>>>(A);
+      break;
+    case ST_CWRITE:
+      if constexpr (BaseItem<DT>::KEY_ONLY) count_write_kernel<DT><<<A.count_grid, CNT_THREADS, 0, tl>>>(A);
+      break;
     case ST_NEXT: driver_kernel<DT, ALGO><<<1, PLAN_THREADS, 0, tl>>>(ctl, 2); break;
   }
 }
@@ -566,6 +585,8 @@ __device__ void plan_round(SortCtl *ctl, bool launch) {
     ctl->deferred += p - q;
     ctl->counters[1] = 0;
     ctl->counters[8] = 0;
+    ctl->counters[9] = 0;
+    ctl->counters[10] = 0;
     if (r < MAX_ROUNDS) {
       ctl->tasks_per_round[r] = q;
       ctl->elems_per_round[r] = N;

@@ -136,7 +136,8 @@ __device__ __forceinline__ void digit_setup(LevelTask &L) {
 // when the sample covers a good part of them (every key then falls into a
 // slot without clamping).
 template <class Key>
-__device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *cand, int u, int l) {
+__device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *cand, int u, int l,
+                          const Key *samp, int m) {
   const Key tlo = key_from_words<Key>(L.t.lo), thi = key_from_words<Key>(L.t.hi);
   Key llo = key_from_words<Key>(L.lut_lo), lhi = key_from_words<Key>(L.lut_hi);
   if (llo < tlo) llo = tlo;
@@ -150,16 +151,8 @@ __device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *c
   const int lbits = (int)L.lut_bits;
   int ls = bitlen((Key)(lhi - llo)) - lbits;
   if (ls < 0) ls = 0;
-  const u32 nlut = (u32)((lhi - llo) >> ls) + 1;
   const int nspl = (1 << l) - 1;
   const int eq = (int)L.equality;
-  __syncthreads();  // (all threads have read lut_lo / lut_hi)
-  if (threadIdx.x == 0) {
-    key_to_words<Key>(llo, L.lut_lo);
-    L.lut_ls = (u32)ls;
-    L.lut_n = nlut;
-    L.lut_span = span ? 1u : 0u;
-  }
   auto lower = [&](Key v) -> u32 {  // #{spl[i] < v, i < s}
     u32 a = 0, b = (u32)nspl;
     while (a < b) {
@@ -169,12 +162,64 @@ __device__ void build_lut(const LevelArgs &A, LevelTask &L, int ti, const Key *c
     }
     return a;
   };
+  // Two slot mappings (lut_slot_of): linear over [llo, lhi], or logarithmic
+  // with M = lut_bits - 6 mantissa bits (fits: 2^M (65 - M) <= 2^lut_bits).
+  // The table the classification uses is the one whose slots make the
+  // sample's keys cheaper to classify: a sample key in a slot without a
+  // splitter (or a one-key slot) costs nothing, one with c splitters
+  // 1 + log2(c) comparisons (Zipf's splitters crowd the low end
+  // of the range, where the linear slots hold up to 63 of them).
+  const int logm = lbits >= 8 ? lbits - 6 : 0;
+  const u32 nlin = (u32)((lhi - llo) >> ls) + 1;
+  const u32 nlog = logm ? lut_slot_of((u64)(lhi - llo), 0, logm) + 1 : 0;
+  auto slot_range = [&](u32 q, u32 n, int lm, Key &r0, Key &r1) {
+    r0 = q == 0 ? tlo : llo + (Key)lut_slot_start(q, ls, lm);
+    r1 = q + 1 == n ? thi : llo + (Key)lut_slot_start(q + 1, ls, lm) - 1;
+  };
+  auto cost = [&](Key x, u32 n, int lm) -> u32 {
+    const u32 q = x < llo ? 0u : min(lut_slot_of((u64)(x - llo), ls, lm), n - 1);
+    Key r0, r1;
+    slot_range(q, n, lm, r0, r1);
+    const u32 a = lower(r0), b = r1 == key_max<Key>() ? (u32)nspl : lower(r1 + 1);
+    if (b == a || r0 == r1) return 0u;
+    return b - a == 1 ? 1u : 1u + (u32)bitlen((u64)(b - a - 1));
+  };
+  __shared__ unsigned long long s_cost[2];
+  if (threadIdx.x == 0) s_cost[0] = s_cost[1] = 0;
+  __syncthreads();  // (all threads have read lut_lo / lut_hi)
+  // (every 4th sample: the costs are estimates; the linear table is kept
+  // without evaluating the other when it already resolves almost every key
+  // without a comparison -- uniform keys)
+  constexpr int CSTRIDE = 4;
+  if (logm) {
+    unsigned long long c0 = 0;
+    for (int i = threadIdx.x * CSTRIDE; i < m; i += blockDim.x * CSTRIDE) c0 += cost(samp[i], nlin, 0);
+    atomicAdd(&s_cost[0], c0);
+  }
+  __syncthreads();
+  const bool try_log = logm && s_cost[0] * 16 * CSTRIDE > (unsigned long long)m;
+  if (try_log) {
+    unsigned long long c1 = 0;
+    for (int i = threadIdx.x * CSTRIDE; i < m; i += blockDim.x * CSTRIDE) c1 += cost(samp[i], nlog, logm);
+    atomicAdd(&s_cost[1], c1);
+  }
+  __syncthreads();
+  const bool use_log = try_log && 5 * s_cost[1] < 4 * s_cost[0];  // (a clear gain only)
+  const int lm = use_log ? logm : 0;
+  const u32 nlut = use_log ? nlog : nlin;
+  if (threadIdx.x == 0) {
+    key_to_words<Key>(llo, L.lut_lo);
+    L.lut_ls = (u32)ls;
+    L.lut_n = nlut;
+    L.lut_span = span ? 1u : 0u;
+    L.lut_log = (u32)lm;
+  }
   unsigned short *lut = A.luts + L.lut_off;
   for (u32 q = threadIdx.x; q < (1u << lbits); q += blockDim.x) {
     u32 e = 0;
     if (q < nlut) {
-      const Key r0 = q == 0 ? tlo : llo + ((Key)q << ls);
-      const Key r1 = q + 1 == nlut ? thi : llo + (((Key)(q + 1)) << ls) - 1;
+      Key r0, r1;
+      slot_range(q, nlut, lm, r0, r1);
       // a = #{splitters < r0}; the count covers splitters in [r0, r1] (a slot
       // with none cannot hold a key equal to a splitter: key < s_a, except
       // above the last splitter -- bucket 2s+1 with equality buckets)
@@ -461,7 +506,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
     int rank = (2 * p + 1) * (1 << (l - 1 - d)) - 1;
     tree[i] = s_cand[rank < u ? rank : u - 1];
   }
-  if constexpr (Tr::D <= 16) build_lut<Key>(A, L, ti, s_cand, u, l);
+  if constexpr (Tr::D <= 16) build_lut<Key>(A, L, ti, s_cand, u, l, s_keys, m);
   (void)s;
 }
 

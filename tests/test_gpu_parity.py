@@ -35,6 +35,27 @@ def ips():
 
 def make(dtype, n, seed, kind="uniform"):
     rng = np.random.default_rng(seed)
+    if kind == "zipf":  # Zipf ranks (the splitters crowd the low end: logarithmic lookup table)
+        z = gen.zipf_u64(n, seed)
+        if dtype == U64:
+            return z
+        if dtype == F64:
+            return z.astype(np.float64) * 0.5
+        if dtype == U32:
+            return z.astype(np.uint32)
+        if dtype == PAIR:
+            p = gen.pairs(n, seed)
+            p[:, 0] = z
+            return p
+        if dtype == QUARTET:
+            q = gen.quartets(n, seed)
+            q[:, 0] = 0
+            q[:, 1] = z
+            return q
+        r = gen.records100(n, seed)
+        r[:, :10] = 0
+        r[:, 6:10] = z.astype(">u4").view(np.uint8).reshape(-1, 4)
+        return r
     if dtype == QUARTET:
         q = gen.quartets(n, seed)
         if kind == "dups":
@@ -124,7 +145,7 @@ def test_device_classifier_matches_oracle(ips, orc, dtype, eq):
 # ----------------------------------------------------------------- one level
 @pytest.mark.parametrize("dtype", [U64, F64, PAIR, REC100, U32, QUARTET])
 @pytest.mark.parametrize("n,kind", [(5003, "uniform"), (100003, "uniform"), (70001, "dups"),
-                                    (40000, "few"), (1 << 20, "uniform")])
+                                    (40000, "few"), (1 << 20, "uniform"), (1 << 20, "zipf")])
 def test_partition_step_tree(ips, orc, dtype, n, kind):
     """K1..K5 of one level: the sampled tree is bit-identical to
     the oracle's recomputation (same counter-based samples); E equals the
@@ -149,6 +170,10 @@ def test_partition_step_tree(ips, orc, dtype, n, kind):
     assert np.array_equal(info["splitter"], o_spl), "splitters differ from the oracle's"
     assert np.array_equal(info["tree"][kb:], o_tree[kb:]), "tree differs from the oracle's"
     assert K == (2 * leaves if eq else leaves)
+    if kind == "zipf" and dtype in (U64, U32, PAIR):
+        assert info["lut_log"] > 0, "Zipf keys should take the logarithmic lookup table"
+    if kind == "uniform" and n >= (1 << 20):
+        assert info["lut_log"] == 0
     # K3 parity: E equals the oracle histogram prefix with these splitters
     spl_el = splitters_as_elements(info["splitter"], dtype, leaves)
     hist = orc.histogram(a, dtype, spl_el, l, eq)
@@ -301,6 +326,41 @@ def test_narrow_range_counting_base_case(ips, orc, dtype, nvals):
         a = np.where(v % 2 == 0, 1.0 + (v // 2) * ulp, -(1.0 + (v // 2) * ulp)).astype(np.float64)
     g, st = gpu_sort(a, dtype, base_cap=1000)
     check(orc, a, g, dtype)
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, U32])
+@pytest.mark.parametrize("kind", ["random", "rootdup", "edge"])
+def test_count_first_narrow_tasks(ips, orc, dtype, kind):
+    """Children larger than the base case whose key range holds at most 4096
+    values are counted and written from the counts (k_count.cuh): 2^25 keys
+    over ~1000 values give level-1 buckets of ~131K elements and a few values
+    each.  'edge' puts the values at the top of the key range (lo + v near
+    the maximum key) and mixes in a wide tail so that some buckets are not
+    narrow."""
+    n = (1 << 25) + 5
+    rng = np.random.default_rng(17)
+    if kind == "random":
+        v = rng.integers(0, 1000, n)
+    elif kind == "rootdup":
+        v = np.arange(n) % 1024
+    else:
+        v = rng.integers(0, 3000, n)
+    if dtype == U64:
+        a = v.astype(np.uint64) + (np.uint64(2**64 - 4000) if kind == "edge" else np.uint64(7 << 33))
+        if kind == "edge":
+            a[: n // 8] = gen.uniform_u64(n // 8, 5)
+    elif dtype == U32:
+        a = (v + (2**32 - 4000 if kind == "edge" else 99)).astype(np.uint32)
+        if kind == "edge":
+            a[: n // 8] = gen.uniform_u32(n // 8, 5)
+    else:
+        ulp = np.float64(2.0**-52)
+        a = np.where(v % 2 == 0, 3.0 + (v // 2) * 2 * ulp, -(3.0 + (v // 2) * 2 * ulp)).astype(np.float64)
+        if kind == "edge":
+            a[: n // 8] = gen.uniform_f64(n // 8, 5)
+    g, st = gpu_sort(a, dtype)
+    check(orc, a, g, dtype)
+    assert st["basecase_elems"] + st["equal_elems"] <= n
 
 
 def _patterns(n, rng):

@@ -30,4 +30,4 @@ for r in range(reps + 3):
         ts.append(e0.elapsed_time(e1))
 w = work.cpu().numpy().view(np.uint64)
 assert np.all(w[1:] >= w[:-1])
-print(f"{sys.argv[1].split('/')[-3]:>22s} n=2^{n.bit_length()-1}: mean {np.mean(ts):.3f} ms  min {np.min(ts):.3f}  -> {n/np.mean(ts)/1e6:.2f} Gkeys/s", flush=True)
+print(f"{sys.argv[1].split('/')[-1]:>22s} n=2^{n.bit_length()-1}: mean {np.mean(ts):.3f} ms  min {np.min(ts):.3f}  -> {n/np.mean(ts)/1e6:.2f} Gkeys/s", flush=True)
