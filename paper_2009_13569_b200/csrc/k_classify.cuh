@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     s_tcnt[j] = 0;
     s_cnt[j] = 0;
   }
+  if (tid == 0) s_ws[KI / 32] = 0;  // block allocator of the first tile
   u32 myfill = 0;  // tid < KI: elements buffered for bucket tid
 
   // Lookup table of starting leaves, built once per task by K1
@@ -528,14 +529,35 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     for (int k = 0; k < IPT; ++k)
       if (sl[k] != NONE && IPS4O_GUARD(sl[k] < (u32)(KI * BUFS), A.err)) s_buf[sl[k]] = xl[k];
 
-    // ---- plan: nb blocks per bucket; scan of (nb | staged blocks << 16)
-    u32 nb = 0, boff = 0, soff = 0;
+    // ---- plan: nb blocks per bucket.  The buckets that emit blocks take
+    //      their block indices and staged runs with ONE atomic on the packed
+    //      total (nb | staged blocks << 16): the order of a tile's blocks in
+    //      the stripe is free (their buckets are recorded per block, K4 reads
+    //      them), so no scan and no second barrier is needed.
+#ifndef IPS4O_CLS_SCAN_PLAN
     if (tid < KI) {
       const u32 tc = s_tcnt[tid];
       s_tcnt[tid] = 0;
       s_cnt[tid] += tc;
       const u32 tot = myfill + tc;
-      nb = tot / B;
+      const u32 nb = tot / B;
+      u32 pl = myfill;
+      if (nb) {
+        const u32 pre = atomicAdd(&s_ws[KI / 32], nb | ((nb - 1) << 16));
+        const u32 boff = pre & 0xFFFFu, soff = pre >> 16;
+        pl |= ((nb * B) << 8) | (soff << 21);
+        for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
+      }
+      s_plan[tid] = pl;
+      myfill = tot - nb * B;
+    }
+#else
+    if (tid < KI) {
+      const u32 tc = s_tcnt[tid];
+      s_tcnt[tid] = 0;
+      s_cnt[tid] += tc;
+      const u32 tot = myfill + tc;
+      const u32 nb = tot / B;
       const u32 pv = nb | ((nb ? nb - 1 : 0u) << 16);
       u32 incl = pv;
 #pragma unroll
@@ -548,13 +570,13 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       const u32 wv = lane < KI / 32 ? s_ws[lane] : 0u;
       const u32 wpre = __reduce_add_sync(0xffffffffu, lane < wid ? wv : 0u);
       const u32 pre = wpre + incl - pv;
-      boff = pre & 0xFFFFu;
-      soff = pre >> 16;
+      const u32 boff = pre & 0xFFFFu, soff = pre >> 16;
       s_plan[tid] = myfill | ((nb * B) << 8) | (soff << 21);
       for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
       if (tid == KI - 1) s_ws[KI / 32] = pre + pv;  // totals
       myfill = tot - nb * B;
     }
+#endif
     __syncthreads();  // B: plan visible
     const u32 nblocks = s_ws[KI / 32] & 0xFFFFu;
 
@@ -575,7 +597,10 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       sl[k] = (valid && !keep) ? j * BUFS + (v - cut) : NONE;
       xl[k] = x[k];
     }
-    __syncthreads();  // C: blocks complete
+    __syncthreads();  // C: blocks complete (everyone has read the totals)
+#ifndef IPS4O_CLS_SCAN_PLAN
+    if (tid == 0) s_ws[KI / 32] = 0;  // the next tile's block allocator
+#endif
 
     // ---- copy the emitted blocks to the stripe's write front; bucket j's
     //      blocks are [boff_j, boff_j + nb_j): block 0 from buffer j, the
