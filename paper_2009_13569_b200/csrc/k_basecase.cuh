@@ -293,6 +293,14 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   using Key = typename BI::Key;
   using S = BaseSmem<DT>;
   constexpr int NT = BI::THREADS, D = Tr::D;
+  // runs of 2..RL elements are sorted by one thread (phase 5: a network over
+  // the run list), longer ones by a warp.  (RL = 8 with a 19-comparator
+  // network for 8-byte items measured slower: 26.4 -> 27.0 ms at 2^30, the
+  // 8-item registers spill and every warp pays the longer network)
+#ifndef IPS4O_BC_RL
+#define IPS4O_BC_RL 4
+#endif
+  constexpr int RL = (SPLITK || sizeof(typename BI::Item) > 8) ? RW + 1 : IPS4O_BC_RL;
   extern __shared__ __align__(16) char smem[];
   Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
   char *s_rec = smem + S::off_rec;
@@ -358,7 +366,15 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     P.nd = direct ? (int)r32 + 1 : (1 << lg);
     P.direct = direct;
     P.exact = direct && ds == 0;  // a digit holds a single key value
-    P.dmul = direct ? 1u : (u32)((1ull << (32 + lg)) / ((u64)r32 + 1));
+    // dmul = floor(2^(32+lg) / (r32 + 1)) (digits < 2^lg): one double
+    // division and a correction instead of a 64-bit integer division (thread
+    // 0 computes it while the CTA waits at the next barrier)
+    u64 dm = 1;
+    if (!direct) {
+      dm = (u64)(ldexp(1.0, 32 + lg) / (double)((u64)r32 + 1));
+      if (dm * ((u64)r32 + 1) > (1ull << (32 + lg))) --dm;
+    }
+    P.dmul = (u32)dm;
   };
   u32 tdw = 0;
   if (blockIdx.x < count) {
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     // 2. exclusive scan in place: thread t owns the WPT consecutive words
     //    [t*WPT, (t+1)*WPT) (vector loads), one block-wide scan of the thread
     //    totals.  Each word becomes (start(2w), start(2w+1)).
+    u32 run_off = 0, nruns = 0;  // short runs (2..RW+1 elements): this thread's list offset, total
     if (hbig) {
       // exact counters (no long runs): warp wi scans the word segment
       // [wi*seg, (wi+1)*seg) row by row (lane l reads word row + l: no bank
@@ -524,23 +541,32 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #pragma unroll
         for (int q = 0; q < WPT; ++q) h[q] = s_hist[tid * WPT + q];
       }
-      u32 tot = 0;
+      u32 tot = 0, nr = 0;
+      auto short_run = [](u32 c) -> u32 { return (c >= 2u && c <= (u32)RL) ? 1u : 0u; };
 #pragma unroll
-      for (int q = 0; q < WPT; ++q) tot += (h[q] & 0xFFFFu) + (h[q] >> 16);
+      for (int q = 0; q < WPT; ++q) {
+        tot += (h[q] & 0xFFFFu) + (h[q] >> 16);
+        nr += short_run(h[q] & 0xFFFFu) + short_run(h[q] >> 16);
+      }
+      // one scan for both: elements (low half; <= CAP < 2^16) and short runs
+      // (high half; <= 2^13) -- the run list offsets of phase 5
       u32 all;
-      u32 st = block_exclusive_scan<NT>(tot, s_ws, &all);
+      const u32 pre = block_exclusive_scan<NT>(tot | (nr << 16), s_ws, &all);
+      u32 st = pre & 0xFFFFu;
+      run_off = pre >> 16;
+      nruns = all >> 16;
 #pragma unroll
       for (int q = 0; q < WPT; ++q) {
         const u32 c0 = h[q] & 0xFFFFu, c1 = h[q] >> 16;
         const u32 w = (u32)(tid * WPT + q);
-        // runs longer than RW + 1 are listed for the warp sort
-        if (!exact && (c0 > RW + 1 || c1 > RW + 1) && w < (u32)nw) {
-          if (c0 > RW + 1) {
+        // runs longer than RL are listed for the warp sort
+        if (!exact && (c0 > (u32)RL || c1 > (u32)RL) && w < (u32)nw) {
+          if (c0 > (u32)RL) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w;
             if (c0 > RANKMAX) atomicAdd(&s_bigsum, c0);
           }
-          if (c1 > RW + 1) {
+          if (c1 > (u32)RL) {
             const u32 slot = atomicAdd(&s_nbig, 1u);
             if (slot < BIGCAP) s_big[slot] = 2u * w + 1u;
             if (c1 > RANKMAX) atomicAdd(&s_bigsum, c1);
@@ -692,40 +718,121 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
           for (int d = dlo + wid; d < dhi; d += NT / 32) {
             const int a = d ? (int)s_end[d - 1] : 0;
             const int n = (int)s_end[d] - a;
-            if (n > RW + 1) warp_sort_run<BI>(s_items + (a - off), n, lane);
+            if (n > RL) warp_sort_run<BI>(s_items + (a - off), n, lane);
           }
         }
         if (nbig) __syncthreads();
       }
       BC_PHASE(4)
-      // 5. rank inside the run by counting (independent compares, so warps
-      //    keep several loads in flight), write to the final position
-      for (int i = tid; i < mp; i += NT) {
-        const Item it = s_items[i];
-        const u32 d = digit(it);
-        const int a = (d ? (int)s_end[d - 1] : 0) - off;
-        const int b = (int)s_end[d] - off;
-        int rank = i - a;
-        if (!exact && !whole && b - a > 1 && b - a <= RW + 1) {
-          // the run lies inside [i - RW, i + RW]: a fixed, branch-free window
-          // (ties by position)
-          rank = 0;
+      if constexpr (!SPLITK) {
+        // 5. runs of 2..RW+1 elements, sorted from a dense list: each thread
+        //    re-reads the run ends of its scan words, then (once every
+        //    thread has read them) writes its short runs (start | count << 16)
+        //    into the counter area at its scan offset; thread r then sorts
+        //    runs r, r + NT, ... (neighbouring threads, neighbouring runs) by
+        //    a 4-input network whose comparators past the run are skipped --
+        //    the parallel form of the paper's insertion-sort base case
+        //    (P:1652).  No thread works on a run of one element.
+        constexpr int WPT = ((1 << BI::DBMAX) / 2 + NT - 1) / NT;
+        static_assert(RW + 1 == 4 && (RL == 4 || RL == 8), "4- and 8-input networks");
+        if (!exact && !whole && nruns > 0) {
+          u32 he[WPT];
 #pragma unroll
-          for (int o = -RW; o <= RW; ++o) {
-            const int j = i + o;
-            if (o != 0 && j >= a && j < b) {
-              const Item y = s_items[j];
-              rank += (o < 0 ? !BI::less(it, y) : BI::less(y, it)) ? 1 : 0;
+          for (int q = 0; q < WPT; ++q) he[q] = s_hist[tid * WPT + q];
+          u32 prev = tid ? (s_hist[tid * WPT - 1] >> 16) : 0u;  // end of the digit before this thread's
+          __syncthreads();  // (every thread has read its run ends)
+          u32 *s_runs = s_hist;
+          u32 k = run_off;
+#pragma unroll
+          for (int q = 0; q < WPT; ++q) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const u32 b = hh ? he[q] >> 16 : he[q] & 0xFFFFu;
+              const u32 c = b - prev;
+              if (c >= 2u && c <= (u32)RL) s_runs[k++] = prev | (c << 16);
+              prev = b;
             }
           }
+          __syncthreads();
+          for (u32 r = tid; r < nruns; r += NT) {
+            const u32 e = s_runs[r];
+            const int a = (int)(e & 0xFFFFu), c = (int)(e >> 16);
+            Item v[RL];
+#pragma unroll
+            for (int u = 0; u < RL; ++u)
+              if (u < c) v[u] = s_items[a + u];
+            auto cx = [&](int i, int j) {
+              if (j < c && BI::less(v[j], v[i])) {
+                const Item t = v[i];
+                v[i] = v[j];
+                v[j] = t;
+              }
+            };
+            if (RL == 4 || c <= 4) {
+              cx(0, 1);
+              cx(2, 3);
+              cx(0, 2);
+              cx(1, 3);
+              cx(1, 2);
+            } else if constexpr (RL == 8) {
+              // 19-comparator 8-input network (checked on all 0-1 inputs of
+              // every length <= 8 with the skipped padding comparators)
+              cx(0, 2), cx(1, 3), cx(4, 6), cx(5, 7);
+              cx(0, 4), cx(1, 5), cx(2, 6), cx(3, 7);
+              cx(0, 1), cx(2, 3), cx(4, 5), cx(6, 7);
+              cx(2, 4), cx(3, 5);
+              cx(1, 4), cx(3, 6);
+              cx(1, 2), cx(3, 4), cx(5, 6);
+            }
+#pragma unroll
+            for (int u = 0; u < RL; ++u)
+              if (u < c) s_items[a + u] = v[u];
+          }
+          __syncthreads();
         }
-        const int pos = off + a + rank;
-        if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
-          if (IPS4O_GUARD(pos >= 0 && pos < m, sp.err)) reinterpret_cast<Item *>(g)[pos] = it;
-        } else if constexpr (DT == DT_F64) {
-          reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
-        } else {
-          s_sidx[pos] = (unsigned short)(it & (Item)0xFFFF);
+        // 6. the bucket is sorted in shared memory: coalesced copy out
+#pragma unroll 4
+        for (int i = tid; i < m; i += NT) {
+          const Item it = s_items[i];
+          if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
+            reinterpret_cast<Item *>(g)[i] = it;
+          } else if constexpr (DT == DT_F64) {
+            reinterpret_cast<u64 *>(g)[i] = key_to_f64(it);
+          } else {
+            s_sidx[i] = (unsigned short)(it & (Item)0xFFFF);
+          }
+        }
+      } else {
+        // 5. (split passes) rank inside the run by counting (independent
+        //    compares, so warps keep several loads in flight), write to the
+        //    final position
+        for (int i = tid; i < mp; i += NT) {
+          const Item it = s_items[i];
+          const u32 d = digit(it);
+          const int a = (d ? (int)s_end[d - 1] : 0) - off;
+          const int b = (int)s_end[d] - off;
+          int rank = i - a;
+          if (!exact && !whole && b - a > 1 && b - a <= RW + 1) {
+            // the run lies inside [i - RW, i + RW]: a fixed, branch-free window
+            // (ties by position)
+            rank = 0;
+#pragma unroll
+            for (int o = -RW; o <= RW; ++o) {
+              const int j = i + o;
+              if (o != 0 && j >= a && j < b) {
+                const Item y = s_items[j];
+                rank += (o < 0 ? !BI::less(it, y) : BI::less(y, it)) ? 1 : 0;
+              }
+            }
+          }
+          const int pos = off + a + rank;
+          if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
+            if (IPS4O_GUARD(pos >= 0 && pos < m, sp.err)) reinterpret_cast<Item *>(g)[pos] = it;
+          } else if constexpr (DT == DT_F64) {
+            reinterpret_cast<u64 *>(g)[pos] = key_to_f64(it);
+          } else {
+            s_sidx[pos] = (unsigned short)(it & (Item)0xFFFF);
+          }
         }
       }
       if constexpr (BI::STAGE_RECORDS) {
