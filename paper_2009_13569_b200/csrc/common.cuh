@@ -455,4 +455,30 @@ __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32 *ws, u32 *total) 
   return pre;
 }
 
+// Block-wide exclusive scan with ONE barrier: every warp scans the warp
+// totals itself.  The caller must pass a barrier before `ws` is written again
+// (block_exclusive_scan above ends with one for that).
+template <int NT>
+__device__ __forceinline__ u32 block_exclusive_scan_1b(u32 v, u32 *ws, u32 *total) {
+  static_assert(NT / 32 <= 32, "one warp total per lane");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u32 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  const u32 w = lane < NT / 32 ? ws[lane] : 0u;
+  u32 iw = w;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, iw, o);
+    if (lane >= o) iw += y;
+  }
+  *total = __shfl_sync(0xffffffffu, iw, NT / 32 - 1);
+  return __shfl_sync(0xffffffffu, iw - w, wid) + x - v;
+}
+
 }  // namespace ips4o

@@ -301,6 +301,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #define IPS4O_BC_RL 4
 #endif
   constexpr int RL = (SPLITK || sizeof(typename BI::Item) > 8) ? RW + 1 : IPS4O_BC_RL;
+  // the run-list phase 5 (measured faster than the rank window for 8-byte
+  // keys: 2^30 u64 base case 9.0 -> 8.6 ms; slower for pairs, u32 and
+  // quartets, which keep the window)
+  constexpr bool RUNLIST = !SPLITK && (DT == DT_U64 || DT == DT_F64);
   extern __shared__ __align__(16) char smem[];
   Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
   char *s_rec = smem + S::off_rec;
@@ -476,13 +480,40 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #define IPS4O_BC_BU 4
 #endif
     constexpr int BU = IPS4O_BC_BU;
-    for (int i0 = tid; i0 < m; i0 += NT * BU) {
-      Item it[BU];
+    auto load_batch = [&](Item (&it)[BU], int i0) {
 #pragma unroll
       for (int u = 0; u < BU; ++u) {
         const int i = i0 + u * NT;
         if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
       }
+    };
+#ifndef IPS4O_BC_PIPE
+#define IPS4O_BC_PIPE 0  // (measured: 26.2 -> 27.0 ms with 4, 26.7 with 2 per batch: spills)
+#endif
+#if IPS4O_BC_PIPE
+    // software-pipelined: the next batch's loads (from L2) are in flight
+    // while this batch's digits are counted
+    {
+      Item cur[BU];
+      load_batch(cur, tid);
+      for (int i0 = tid; i0 < m; i0 += NT * BU) {
+        Item nxt[BU];
+        if (i0 + NT * BU < m) load_batch(nxt, i0 + NT * BU);
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+          if (i0 + u * NT < m) {
+            const u32 d = digit(cur[u]);
+            atomicAdd(&s_hist[d >> 1], 1u << ((d & 1) << 4));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < BU; ++u) cur[u] = nxt[u];
+      }
+    }
+#else
+    for (int i0 = tid; i0 < m; i0 += NT * BU) {
+      Item it[BU];
+      load_batch(it, i0);
 #pragma unroll
       for (int u = 0; u < BU; ++u) {
         if (i0 + u * NT < m) {
@@ -491,6 +522,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         }
       }
     }
+#endif
     publish_next();
     __syncthreads();
     BC_PHASE(1)
@@ -511,7 +543,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       for (int w = s0 + lane; w < s1; w += 32) wtot += (s_hist[w] & 0xFFFFu) + (s_hist[w] >> 16);
       wtot = __reduce_add_sync(0xffffffffu, wtot);
       u32 all;
-      u32 carry = __shfl_sync(0xffffffffu, block_exclusive_scan<NT>(lane == 0 ? wtot : 0u, s_ws, &all), 0);
+      u32 carry = __shfl_sync(0xffffffffu, block_exclusive_scan_1b<NT>(lane == 0 ? wtot : 0u, s_ws, &all), 0);
       for (int row = s0; row < s1; row += 32) {
         const int w = row + lane;
         const u32 h = w < s1 ? s_hist[w] : 0u, c0 = h & 0xFFFFu, t = c0 + (h >> 16);
@@ -546,12 +578,12 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < WPT; ++q) {
         tot += (h[q] & 0xFFFFu) + (h[q] >> 16);
-        nr += short_run(h[q] & 0xFFFFu) + short_run(h[q] >> 16);
+        if constexpr (RUNLIST) nr += short_run(h[q] & 0xFFFFu) + short_run(h[q] >> 16);
       }
       // one scan for both: elements (low half; <= CAP < 2^16) and short runs
       // (high half; <= 2^13) -- the run list offsets of phase 5
       u32 all;
-      const u32 pre = block_exclusive_scan<NT>(tot | (nr << 16), s_ws, &all);
+      const u32 pre = block_exclusive_scan_1b<NT>(tot | (nr << 16), s_ws, &all);  // (s_ws is next written after this bucket's barriers)
       u32 st = pre & 0xFFFFu;
       run_off = pre >> 16;
       nruns = all >> 16;
@@ -654,13 +686,18 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       //    again, from L2; items of part B go to the scratch); afterwards the
       //    counters of the pass's digits hold the run ENDS
       if (pass == 0) {
+#if IPS4O_BC_PIPE
+        Item it[BU];
+        load_batch(it, tid);
+#endif
         for (int i0 = tid; i0 < m; i0 += NT * BU) {
+#if IPS4O_BC_PIPE
+          Item nxt[BU];
+          if (i0 + NT * BU < m) load_batch(nxt, i0 + NT * BU);
+#else
           Item it[BU];
-#pragma unroll
-          for (int u = 0; u < BU; ++u) {
-            const int i = i0 + u * NT;
-            if (i < m) it[u] = BI::load(BI::STAGE_RECORDS ? s_rec + (size_t)i * D : g + (size_t)i * D, (u32)i);
-          }
+          load_batch(it, i0);
+#endif
 #pragma unroll
           for (int u = 0; u < BU; ++u) {
             if (i0 + u * NT < m) {
@@ -675,6 +712,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
               }
             }
           }
+#if IPS4O_BC_PIPE
+#pragma unroll
+          for (int u = 0; u < BU; ++u) it[u] = nxt[u];
+#endif
         }
       } else if constexpr (SPLITK) {
         for (int i = tid; i < mp; i += NT) {
@@ -724,7 +765,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         if (nbig) __syncthreads();
       }
       BC_PHASE(4)
-      if constexpr (!SPLITK) {
+      if constexpr (RUNLIST) {
         // 5. runs of 2..RW+1 elements, sorted from a dense list: each thread
         //    re-reads the run ends of its scan words, then (once every
         //    thread has read them) writes its short runs (start | count << 16)

@@ -16,7 +16,7 @@ from collections import OrderedDict, defaultdict
 FAMILY = [
     ("prepass", r"prepass"), ("sample", r"sample_kernel"), ("classify", r"classify"),
     ("boundaries", r"boundaries"), ("stripe_fix", r"stripe_fix"), ("permute", r"permute"),
-    ("cleanup", r"cleanup"), ("schedule", r"schedule"), ("basecase", r"basecase"),
+    ("cleanup", r"cleanup"), ("schedule", r"schedule"), ("basecase", r"basecase|count_"),
     ("reverse", r"reverse"), ("plan", r"entry_kernel|driver_kernel"),
 ]
 
