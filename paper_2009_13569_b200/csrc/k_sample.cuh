@@ -8,11 +8,15 @@ namespace ips4o {
 
 constexpr int SAMPLE_THREADS = 1024;  // = SORT_THREADS
 // at most 16 keys per thread of the register sort (4 for 16-byte keys)
-template <int DT> __host__ __device__ constexpr int sample_max() { return Traits<DT>::D >= 32 ? 4096 : 16384; }
+// (records: 8192, i.e. alpha = 64 at their k = 128, so that level-2 buckets
+// stay below the 1 792-record base case -- records have no split pass)
+template <int DT> __host__ __device__ constexpr int sample_max() {
+  return Traits<DT>::D == 100 ? 8192 : Traits<DT>::D >= 32 ? 4096 : 16384;
+}
 // dynamic shared memory of sample_kernel: p sample slots + 16-bit digit
 // counters (sized per launch, so levels of small tasks run 2 CTAs per SM)
 template <int DT> __host__ __device__ constexpr size_t sample_smem(size_t p = (size_t)sample_max<DT>()) {
-  return p * sizeof(typename Traits<DT>::Key) + (sizeof(typename Traits<DT>::Key) == 8 ? 16384 : 4096) * 2;
+  return p * sizeof(typename Traits<DT>::Key) + (sizeof(typename Traits<DT>::Key) == 8 ? 16384 : Traits<DT>::D == 100 ? 8192 : 4096) * 2;
 }
 
 __host__ __device__ __forceinline__ int next_pow2_i(int x) {
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NT = SAMPLE_THREADS;
   constexpr int MAXE = sample_max<DT>() / NT;
-  constexpr int DB = sizeof(Key) == 8 ? 14 : 12;  // digit bits: 2^DB >= sample_max
+  constexpr int DB = sizeof(Key) == 8 ? 14 : Tr::D == 100 ? 13 : 12;  // digit bits: 2^DB >= sample_max
   static_assert((1 << DB) >= sample_max<DT>(), "one digit per sample");
   constexpr int RUNMAX = 32;                       // longer runs: full sort instead
 
@@ -420,6 +424,8 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
           if constexpr (sizeof(Key) == 8) {
             if (P == 8 * SORT_THREADS) bitonic_sort_reg<Key, 8>(s_keys);
             else bitonic_sort_reg<Key, 16>(s_keys);
+          } else if constexpr (Tr::D == 100) {
+            bitonic_sort_reg<Key, 8>(s_keys);  // P <= 8192
           }
           break;
       }
