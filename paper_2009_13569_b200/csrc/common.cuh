@@ -328,6 +328,19 @@ __device__ __forceinline__ void prefetch_l2(const void *p, u64 bytes, int tid, i
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + off), "r"(sz) : "memory");
   }
 }
+// Bulk (TMA) copy shared -> global of `bytes` (multiple of 16, both addresses
+// 16-byte aligned), issued by one thread after a barrier; the generic-proxy
+// writes to shared memory are made visible to the async proxy first.
+__device__ __forceinline__ void bulk_store_s2g(void *gdst, const void *ssrc, u32 bytes) {
+  const u32 sa = (u32)__cvta_generic_to_shared(ssrc);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the source reads of the issued bulk stores are done (shared memory reusable)
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// the issued bulk stores are complete
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }

@@ -105,12 +105,15 @@ constexpr int BIGCAP = 512;  // runs longer than RW + 1 listed per bucket (more:
 template <int DT> struct BaseSmem {
   using BI = BaseItem<DT>;
   static constexpr size_t off_items = 0;
-  static constexpr size_t off_rec = off_items + (size_t)BI::CAP * sizeof(typename BI::Item);
+  // (+2 items: the u64 bulk copy-out shifts the bucket by one item so that
+  // shared and global addresses agree modulo 16 bytes)
+  static constexpr size_t off_rec = off_items + (((size_t)BI::CAP + 2) * sizeof(typename BI::Item) + 15) / 16 * 16;
   static constexpr size_t off_sidx =
       off_rec + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * Traits<DT>::D + 15) / 16 * 16 : 0);
   static constexpr size_t off_hist = off_sidx + (BI::STAGE_RECORDS ? ((size_t)BI::CAP * 2 + 15) / 16 * 16 : 0);
   static constexpr size_t off_big = off_hist + ((size_t)1 << BI::DBMAX) * 2;  // 16-bit counters, two per word
   static constexpr size_t bytes = off_big + (size_t)BIGCAP * 4 + (BI::THREADS / 32 + 4) * 4;
+  static_assert(bytes <= 232448, "227 KB of dynamic shared memory per CTA");
 };
 
 // Warp bitonic sort of a[0..n) in shared memory.  All comparators point the
@@ -305,6 +308,13 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
   // keys: 2^30 u64 base case 9.0 -> 8.6 ms; slower for pairs, u32 and
   // quartets, which keep the window)
   constexpr bool RUNLIST = !SPLITK && (DT == DT_U64 || DT == DT_F64);
+  // copy-out of the sorted bucket by one bulk (TMA) store instead of a
+  // thread loop; the next bucket's histogram overlaps it
+#ifndef IPS4O_BC_BULK
+#define IPS4O_BC_BULK 1
+#endif
+  constexpr bool BULK = IPS4O_BC_BULK && RUNLIST && DT == DT_U64;
+  bool pend = false;  // a bulk store may still read s_items (CTA-uniform)
   extern __shared__ __align__(16) char smem[];
   Item *s_items = reinterpret_cast<Item *>(smem + S::off_items);
   char *s_rec = smem + S::off_rec;
@@ -356,7 +366,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       } else if (!direct && ds == 0) {
         // (key-only buckets larger than the item array are then written from
         // the counts alone: no item array at all)
-        const u64 used = BI::KEY_ONLY && mm > BI::CAP ? 0 : (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item);
+        const u64 used = BI::KEY_ONLY && mm > BI::CAP ? 0 : (u64)(mm < BI::CAP ? mm : BI::CAP) * sizeof(Item) + (BULK ? 16 : 0);
         const u64 hb = (((u64)r32 / 2 + 1) * 4 + 15) & ~15ull;  // bytes for r32 + 1 counters
         const u64 hend = S::off_hist + (u64)HSTAT * 4;
         if (hend >= hb && hend - hb >= S::off_items + used) {
@@ -459,6 +469,14 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     const int nw = (nd + 1) >> 1;  // hist words: digit 2w in the low half, 2w+1 in the high half
     u32 *s_hist = reinterpret_cast<u32 *>(smem + par.hoff);
     const bool hbig = nw > HSTAT;  // exact counters beyond the static area
+    if (BULK && pend && par.hoff < (u32)S::off_hist) {
+      // the counters overlap the item array that the last bulk store reads
+      if (tid == 0) bulk_wait_read();
+      pend = false;
+      __syncthreads();
+    }
+    // items of this bucket: s_it[i] <-> g[i], equal addresses modulo 16 B (BULK)
+    Item *const s_it = s_items + (BULK ? (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1) : 0);
     BC_PHASE(7)
     for (int w = tid; w < par.nwz / 4; w += NT) reinterpret_cast<uint4 *>(s_hist)[w] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
@@ -524,6 +542,10 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
     }
 #endif
     publish_next();
+    if (BULK && pend) {  // the scatter below overwrites the items
+      if (tid == 0) bulk_wait_read();
+      pend = false;
+    }
     __syncthreads();
     BC_PHASE(1)
     if (has_next && tid == 0) digit_par(s_task[cur ^ 1], s_par[cur ^ 1]);  // visible after the scan
@@ -706,7 +728,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
                 const int sh = (d & 1) << 4;
                 const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
                 if (IPS4O_GUARD(((old >> sh) & 0xFFFFu) < (u32)(m < BI::CAP ? m : BI::CAP), sp.err))
-                  s_items[(old >> sh) & 0xFFFFu] = it[u];
+                  s_it[(old >> sh) & 0xFFFFu] = it[u];
               } else {
                 scratch[atomicAdd(&s_scnt, 1u)] = it[u];
               }
@@ -723,7 +745,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
           const u32 d = digit(it);
           const int sh = (d & 1) << 4;
           const u32 old = atomicAdd(&s_hist[d >> 1], 1u << sh);
-          s_items[(int)((old >> sh) & 0xFFFFu) - off] = it;
+          s_it[(int)((old >> sh) & 0xFFFFu) - off] = it;
         }
       }
       __syncthreads();
@@ -745,7 +767,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       }
 #endif
       if (whole) {
-        block_bitonic<BI, NT>(s_items, mp);
+        block_bitonic<BI, NT>(s_it, mp);
       } else if (!exact) {
         const int nbig = (int)s_nbig;
         if (nbig <= BIGCAP) {
@@ -753,13 +775,13 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             const int d = (int)s_big[q];
             if (d < dlo || d >= dhi) continue;
             const int a = d ? (int)s_end[d - 1] : 0;
-            warp_sort_run<BI>(s_items + (a - off), (int)s_end[d] - a, lane);
+            warp_sort_run<BI>(s_it + (a - off), (int)s_end[d] - a, lane);
           }
         } else {
           for (int d = dlo + wid; d < dhi; d += NT / 32) {
             const int a = d ? (int)s_end[d - 1] : 0;
             const int n = (int)s_end[d] - a;
-            if (n > RL) warp_sort_run<BI>(s_items + (a - off), n, lane);
+            if (n > RL) warp_sort_run<BI>(s_it + (a - off), n, lane);
           }
         }
         if (nbig) __syncthreads();
@@ -801,7 +823,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             Item v[RL];
 #pragma unroll
             for (int u = 0; u < RL; ++u)
-              if (u < c) v[u] = s_items[a + u];
+              if (u < c) v[u] = s_it[a + u];
             auto cx = [&](int i, int j) {
               if (j < c && BI::less(v[j], v[i])) {
                 const Item t = v[i];
@@ -827,14 +849,27 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             }
 #pragma unroll
             for (int u = 0; u < RL; ++u)
-              if (u < c) s_items[a + u] = v[u];
+              if (u < c) s_it[a + u] = v[u];
           }
           __syncthreads();
         }
         // 6. the bucket is sorted in shared memory: coalesced copy out
+        if constexpr (BULK) {
+          // one bulk store of the 16-byte aligned middle (thread 0, after
+          // every thread's async-proxy fence and a barrier); the unaligned
+          // first / odd last item by single stores
+          const int a0 = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+          const int nb = (m - a0) & ~1;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (tid == 0 && nb > 0) bulk_store_s2g(reinterpret_cast<Item *>(g) + a0, s_it + a0, (u32)nb * (u32)sizeof(Item));
+          if (tid == 32 && a0) reinterpret_cast<Item *>(g)[0] = s_it[0];
+          if (tid == 64 && a0 + nb < m) reinterpret_cast<Item *>(g)[m - 1] = s_it[m - 1];
+          pend = nb > 0;
+        }
 #pragma unroll 4
-        for (int i = tid; i < m; i += NT) {
-          const Item it = s_items[i];
+        for (int i = tid; i < (BULK ? 0 : m); i += NT) {
+          const Item it = s_it[i];
           if constexpr (DT == DT_U64 || DT == DT_PAIR || DT == DT_U32 || DT == DT_QUARTET) {
             reinterpret_cast<Item *>(g)[i] = it;
           } else if constexpr (DT == DT_F64) {
@@ -848,7 +883,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         //    compares, so warps keep several loads in flight), write to the
         //    final position
         for (int i = tid; i < mp; i += NT) {
-          const Item it = s_items[i];
+          const Item it = s_it[i];
           const u32 d = digit(it);
           const int a = (d ? (int)s_end[d - 1] : 0) - off;
           const int b = (int)s_end[d] - off;
@@ -861,7 +896,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             for (int o = -RW; o <= RW; ++o) {
               const int j = i + o;
               if (o != 0 && j >= a && j < b) {
-                const Item y = s_items[j];
+                const Item y = s_it[j];
                 rank += (o < 0 ? !BI::less(it, y) : BI::less(y, it)) ? 1 : 0;
               }
             }
@@ -890,6 +925,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
       BC_PHASE(6)
     }
   }
+  if (BULK && tid == 0) bulk_wait_all();
 #ifdef IPS4O_PHASE_TIMING
   if (tid == 0 && blockIdx.x == 0)
     printf("basecase CTA0 cycles: setup %lld zero %lld hist %lld scan %lld scatter %lld big %lld rank+write %lld endbar %lld\n",

@@ -2,7 +2,7 @@
 duration, DRAM bytes and throughput, issue/occupancy, shared-memory
 wavefronts and conflicts, top stall reasons, registers.
 
-    python tools/ncu_summary.py rep1.ncu-rep [rep2 ...] > profiles/r1_ncu_full_summary.txt
+    python tools/ncu_summary.py rep1.ncu-rep|raw1.csv [...] > profiles/r1_ncu_full_summary.txt
 """
 import csv
 import io
@@ -28,7 +28,10 @@ STALLS = ["barrier", "short_scoreboard", "long_scoreboard", "wait", "math_pipe_t
 
 def main():
     for rep in sys.argv[1:]:
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        if rep.endswith(".csv"):  # an exported `--page raw --csv`
+            raw = open(rep).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         h, units = rows[0], rows[1]
         for r in rows[2:]:
