@@ -534,49 +534,23 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     //      total (nb | staged blocks << 16): the order of a tile's blocks in
     //      the stripe is free (their buckets are recorded per block, K4 reads
     //      them), so no scan and no second barrier is needed.
-#ifndef IPS4O_CLS_SCAN_PLAN
     if (tid < KI) {
-      const u32 tc = s_tcnt[tid];
-      s_tcnt[tid] = 0;
-      s_cnt[tid] += tc;
-      const u32 tot = myfill + tc;
+      // s_tcnt[j] started the tile at bucket j's buffer fill, so the rank
+      // atomics returned each element's position v in the bucket's stream
+      const u32 tot = s_tcnt[tid];
+      s_cnt[tid] += tot - myfill;
       const u32 nb = tot / B;
-      u32 pl = myfill;
+      u32 pl = 0;
       if (nb) {
         const u32 pre = atomicAdd(&s_ws[KI / 32], nb | ((nb - 1) << 16));
         const u32 boff = pre & 0xFFFFu, soff = pre >> 16;
-        pl |= ((nb * B) << 8) | (soff << 21);
+        pl = ((nb * B) << 8) | (soff << 21);
         for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
       }
       s_plan[tid] = pl;
       myfill = tot - nb * B;
+      s_tcnt[tid] = myfill;  // the next tile's ranks start at the new fill
     }
-#else
-    if (tid < KI) {
-      const u32 tc = s_tcnt[tid];
-      s_tcnt[tid] = 0;
-      s_cnt[tid] += tc;
-      const u32 tot = myfill + tc;
-      const u32 nb = tot / B;
-      const u32 pv = nb | ((nb ? nb - 1 : 0u) << 16);
-      u32 incl = pv;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const u32 yv = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += yv;
-      }
-      if (lane == 31) s_ws[wid] = incl;
-      asm volatile("bar.sync 1, %0;" ::"n"(KI) : "memory");
-      const u32 wv = lane < KI / 32 ? s_ws[lane] : 0u;
-      const u32 wpre = __reduce_add_sync(0xffffffffu, lane < wid ? wv : 0u);
-      const u32 pre = wpre + incl - pv;
-      const u32 boff = pre & 0xFFFFu, soff = pre >> 16;
-      s_plan[tid] = myfill | ((nb * B) << 8) | (soff << 21);
-      for (u32 q = 0; q < nb; ++q) s_blkb[boff + q] = (unsigned short)(tid | (q << 9));
-      if (tid == KI - 1) s_ws[KI / 32] = pre + pv;  // totals
-      myfill = tot - nb * B;
-    }
-#endif
     __syncthreads();  // B: plan visible
     const u32 nblocks = s_ws[KI / 32] & 0xFFFFu;
 
@@ -588,8 +562,9 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     for (int k = 0; k < IPT; ++k) {
       const bool valid = cnt == T || tid + k * NT < cnt;
       const u32 j = valid ? bkt[k] : 0u;
-      const u32 pl = s_plan[j];
-      const u32 v = (pl & 0xFFu) + rank[k];
+      const u32 v = rank[k];
+      // only elements past the buffer read the plan (about a quarter)
+      const u32 pl = v >= (u32)B ? s_plan[j] : 0u;
       const u32 cut = (pl >> 8) & 0x1FFFu;
       const u32 pos = v < (u32)B ? j * BUFS + v : STG0 + (pl >> 21) * B + v - B;
       const bool keep = v < cut || v < (u32)B;
@@ -598,9 +573,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
       xl[k] = x[k];
     }
     __syncthreads();  // C: blocks complete (everyone has read the totals)
-#ifndef IPS4O_CLS_SCAN_PLAN
     if (tid == 0) s_ws[KI / 32] = 0;  // the next tile's block allocator
-#endif
 
     // ---- copy the emitted blocks to the stripe's write front; bucket j's
     //      blocks are [boff_j, boff_j + nb_j): block 0 from buffer j, the
