@@ -249,7 +249,11 @@ int ips4o_partition_splitters(void *ptr, uint64_t n, int dtype, void *stream,
  * tree[1..s] / splitter[0..s] with s = 2^l - 1 (tree[0] unused, zero) follow
  * P:402-406.  For IPS4O_ALGO_DIGIT, tree/splitter are untouched and
  * `shift`, `l` (= digit bits) describe the extractor (key >> shift) & (2^l - 1)
- * over the order-preserving 64-bit (or 80-bit) key.
+ * over the order-preserving 64-bit (or 80-bit) key; with lut_log = M > 0 the
+ * sample-adaptive extractor (DESIGN R33) is in use instead: the
+ * bucket of a key is the logarithmic digit of (key - smallest key of A) with
+ * M mantissa bits (offsets below 2^(M+1) map to themselves, every octave
+ * above to 2^M equal slots), shift = 0.
  * Host arrays are caller-owned: E needs room for kidx_max+1 uint64,
  * tree and splitter for kidx_max keys of key_bytes each.  Synchronous. */
 typedef struct ips4o_step_info {
@@ -269,7 +273,8 @@ typedef struct ips4o_step_info {
     void *splitter;        /* [2^l] keys (out, TREE)                              */
     int32_t lut_log;       /* lookup table of starting leaves (TREE, keys <= 16 B):
                               0 = linear slots, M > 0 = logarithmic slots with M
-                              mantissa bits (DESIGN "Classification")          */
+                              mantissa bits (DESIGN "Classification"); DIGIT:
+                              M > 0 = logarithmic digit (see above)             */
     int32_t reserved0;
 } ips4o_step_info;
 int ips4o_partition_step(void *ptr, uint64_t n, int dtype, void *stream,

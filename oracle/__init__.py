@@ -73,6 +73,8 @@ def lib():
         L.orc_classify_tree.restype = ci
         L.orc_radix_digit.argtypes = [ci, vp, ci, ci]
         L.orc_radix_digit.restype = ctypes.c_uint32
+        L.orc_log_digit.argtypes = [ctypes.c_uint64, ci]
+        L.orc_log_digit.restype = ctypes.c_uint32
         L.orc_boundaries.argtypes = [vp, ci, u64, vp, vp]
         L.orc_boundaries.restype = None
         L.orc_histogram.argtypes = [vp, u64, ci, vp, ci, ci, vp]
@@ -192,6 +194,11 @@ def classify_tree(tree: np.ndarray, splitter: np.ndarray, l: int, equality: bool
 def radix_digit(dtype: int, e: np.ndarray, shift: int, bits: int) -> int:
     e = np.ascontiguousarray(e)
     return int(lib().orc_radix_digit(dtype, _ptr(e), shift, bits))
+
+
+def log_digit(d: int, M: int) -> int:
+    """Logarithmic digit of the offset d (DESIGN R33)."""
+    return int(lib().orc_log_digit(int(d), int(M)))
 
 
 def boundaries(count, b: int):

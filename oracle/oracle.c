@@ -490,6 +490,23 @@ uint32_t orc_radix_digit(int dtype, const void *e, int shift, int bits)
     return (uint32_t)d;
 }
 
+/* Logarithmic digit of the sample-adaptive IPS2Ra extractor (P:4042-4047 asks
+ * for an extractor adapted to the input distribution; the mapping itself is
+ * DESIGN.md reading R33): the offset d of a key from its task's lower bound
+ * maps to itself while d < 2^(M+1); an offset with leading bit e > M (2^e <=
+ * d < 2^(e+1)) maps into the octave's 2^M equal slots: the slots of octave e
+ * start at 2^M (e - M + 1) and the offset takes slot number floor((d - 2^e) /
+ * 2^(e-M)) of them.  Monotone, and consecutive slots are contiguous. */
+uint32_t orc_log_digit(uint64_t d, int M)
+{
+    if (d < ((uint64_t)2 << M)) return (uint32_t)d;
+    int e = 0;
+    while (e < 63 && (d >> (e + 1)) != 0) e++; /* leading bit */
+    uint64_t first = ((uint64_t)1 << M) * (uint64_t)(e - M + 1);
+    uint64_t width = (uint64_t)1 << (e - M);
+    return (uint32_t)(first + (d - ((uint64_t)1 << e)) / width);
+}
+
 /* ---------------------------------------------------------------- boundaries */
 
 void orc_boundaries(const uint64_t *count, int k, uint64_t b, uint64_t *E, uint64_t *d)

@@ -108,6 +108,8 @@ int orc_classify_tree(const void *tree, const void *splitter, int l, int equalit
  * key of e.  The key of F64 is obtained by the oracle's own IEEE-754 order
  * argument (DESIGN R20), of REC100 as the 80-bit big-endian number. */
 uint32_t orc_radix_digit(int dtype, const void *e, int shift, int bits);
+/* Logarithmic digit of an offset d (sample-adaptive IPS2Ra extractor, DESIGN R33). */
+uint32_t orc_log_digit(uint64_t d, int M);
 
 /* Bucket boundaries: E[j] = sum_{i<j} count[i] (exact, E[0]=0),
  * d[j] = ceil(E[j]/b)*b (block-rounded delimiters), j = 0..k. */

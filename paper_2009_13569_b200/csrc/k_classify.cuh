@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
   u32 nlut_used = 1;
   bool span_task = false;
   int lut_log = 0;
+  const int dig_log = ALGO == ALGO_DIGIT ? (int)L.lut_log : 0;  // IPS2Ra: logarithmic digit (R33)
   const int nspl = (1 << l) - 1;
   constexpr u32 FIN = LUT_FIN;
   static_assert(KI <= 512, "bucket and splitter indices fit 9 bits");
@@ -493,8 +494,21 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
           }
         }
       } else {
+        if constexpr (sizeof(Key) == 8) {
+          if (dig_log) {
+            // sample-adaptive extractor (k_sample.cuh digit_adapt, DESIGN R33):
+            // logarithmic slots of the offset from the task's lower bound;
+            // the clamp only guards the unused lanes of a partial tile
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+            for (int k = 0; k < IPT; ++k) bkt[k] = min(lut_slot_of((u64)(key[k] - tlo), 0, dig_log), dmask);
+          } else {
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) bkt[k] = digit_of(key[k], shift, dmask);
+        }
       }
     }
     if (cnt == T) {

@@ -177,6 +177,14 @@ __device__ void schedule_task(const LevelArgs &A, u32 ti, const u64 *sE) {
         if (j > 0) lo = spl[j - 1] + 1;
         if (j < s) hi = spl[j];
       }
+    } else if (sizeof(Key) == 8 && L.lut_log) {
+      // logarithmic digit (R33): slot j covers the offsets [start(j), start(j+1))
+      // from the task's lower bound
+      if constexpr (sizeof(Key) == 8) {
+        lo = plo + (Key)lut_slot_start((u32)j, 0, (int)L.lut_log);
+        hi = plo + (Key)lut_slot_start((u32)j + 1, 0, (int)L.lut_log) - 1;
+        if (hi < lo) hi = phi;  // (wrapped past 2^64: the last slots)
+      }
     } else {
       const int bits = (int)L.l;
       const int sb = L.shift + bits;

@@ -406,7 +406,11 @@ __global__ void __launch_bounds__(PERM_THREADS, IPS4O_PERM_MINB) permute_kernel(
           for (int q = 0; q < Tr::KEY_UNITS; ++q) ku[q] = shfl_unit(r[0], q);
         }
         if (lane == 0) {
-          bv = digit_of(Tr::key(reinterpret_cast<const char *>(ku)), shift, dmask);
+          const Key kx = Tr::key(reinterpret_cast<const char *>(ku));
+          bv = digit_of(kx, shift, dmask);
+          if constexpr (sizeof(Key) == 8) {
+            if (L.lut_log) bv = min(lut_slot_of((u64)(kx - key_from_words<Key>(L.t.lo)), 0, (int)L.lut_log), dmask);
+          }
           __nanosleep(PERM_DIGIT_PACE_NS);
         }
       } else {

@@ -131,6 +131,71 @@ __device__ __forceinline__ void digit_setup(LevelTask &L) {
   L.K = 1u << bits;
   L.equality = 0;
   L.k_used = 1u << bits;
+  L.lut_log = 0;
+}
+
+// Sample-adaptive digit extractor of IPS2Ra ("adapting the
+// function for extracting bucket indices to various input distributions
+// (which can be approximated analyzing a sample of the input)"; DESIGN R33).
+// A sample of the task is counted under the plain digit and under the
+// logarithmic slot mapping of the offset from the task's lower bound
+// (lut_slot_of: exact below 2^(M+1), then 2^M slots per octave, M the largest
+// that fits the bucket budget).  When the plain digit puts more than 1/8 of
+// the sample into one bucket and the logarithmic mapping's fullest bucket
+// holds less than half of that, the task is partitioned by the logarithmic
+// mapping (L.lut_log = M); the children return to the plain digit of their
+// own (exact) ranges.  Keys of 8 bytes; bounds must be true bounds of the keys
+// (not TF_LOOSE: offsets are taken from lo).
+#ifndef IPS4O_DIGIT_ADAPT
+#define IPS4O_DIGIT_ADAPT 1
+#endif
+constexpr int DIG_SAMPLE = 2048;
+template <int DT>
+__device__ void digit_adapt(const LevelArgs &A, LevelTask &L) {
+  using Tr = Traits<DT>;
+  using Key = typename Tr::Key;
+  static_assert(sizeof(Key) == 8, "8-byte keys");
+  __shared__ u32 s_h[2][256];
+  __shared__ u32 s_mx[2];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (tid == 0) digit_setup<Key>(L);
+  __syncthreads();
+  if (!IPS4O_DIGIT_ADAPT) return;
+  const Key lo = key_from_words<Key>(L.t.lo), hi = key_from_words<Key>(L.t.hi);
+  const u64 R = (u64)(hi - lo);
+  if ((L.t.flags & TF_LOOSE) || L.t.size < 16 * (u64)DIG_SAMPLE || L.K < 16 || L.k_req > 256 || R < 4096 ||
+      bitlen(R) > 62)
+    return;
+  int M = 0;
+  for (int q = 1; q <= 7; ++q)
+    if (lut_slot_of(R, 0, q) + 1 <= L.k_req) M = q;
+  if (M == 0) return;
+  for (int i = tid; i < 512; i += NT) (&s_h[0][0])[i] = 0;
+  if (tid < 2) s_mx[tid] = 0;
+  __syncthreads();
+  const u32 dmask = L.K - 1;
+  for (int i = tid; i < DIG_SAMPLE; i += NT) {
+    Key x = Tr::key(A.base + sample_index(A.seed, L.t.level, L.t.begin, L.t.size, (u64)i) * Tr::D);
+    x = x < lo ? lo : (x > hi ? hi : x);
+    atomicAdd(&s_h[0][digit_of(x, L.shift, dmask)], 1u);
+    atomicAdd(&s_h[1][min(lut_slot_of((u64)(x - lo), 0, M), 255u)], 1u);
+  }
+  __syncthreads();
+  for (int i = tid; i < 256; i += NT) {
+    atomicMax(&s_mx[0], s_h[0][i]);
+    atomicMax(&s_mx[1], s_h[1][i]);
+  }
+  __syncthreads();
+  if (tid == 0 && s_mx[0] * 8 > (u32)DIG_SAMPLE && s_mx[1] * 2 < s_mx[0]) {
+    const u32 nlog = lut_slot_of(R, 0, M) + 1;
+    u32 K = 2;
+    while (K < nlog) K <<= 1;
+    L.lut_log = (u32)M;
+    L.K = K;
+    L.l = (u32)log2_i((int)K);
+    L.shift = 0;
+    L.k_used = K;
+  }
 }
 
 // The lookup table of starting leaves of a task, built once
@@ -253,7 +318,11 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_kernel(LevelArgs A) {
   const int ti = blockIdx.x;
   LevelTask &L = A.tasks[ti];
   if (ALGO == ALGO_DIGIT) {
-    if (threadIdx.x == 0) digit_setup<Key>(L);
+    if constexpr (sizeof(Key) == 8) {
+      digit_adapt<DT>(A, L);
+    } else {
+      if (threadIdx.x == 0) digit_setup<Key>(L);
+    }
     return;
   }
   extern __shared__ __align__(16) char smem_raw[];

@@ -250,6 +250,52 @@ def test_partition_step_digit(ips, orc, dtype, n):
             assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1
 
 
+@pytest.mark.parametrize("dtype", [U64, U32, PAIR])
+@pytest.mark.parametrize("n", [300007, 1 << 21])
+def test_partition_step_digit_adaptive(ips, orc, dtype, n):
+    """Sample-adaptive IPS2Ra extractor (DESIGN R33): on Zipf keys
+    the plain digit puts most of the sample into bucket 0, so the step uses the
+    logarithmic digit of key - min key (lut_log = M > 0); bucket j holds
+    exactly the elements whose oracle log digit is j, no bucket holds most of
+    the input, and the partition is consistent with the oracle's sort."""
+    a = make(dtype, n, 12, "zipf")
+    t = to_dev(a)
+    info = ips.partition_step(t, dtype, algo=ips.DIGIT, base_cap=2048)
+    g = from_dev(t, a)
+    E = info["E"]
+    K, M = info["num_buckets"], info["lut_log"]
+    assert M > 0 and info["shift"] == 0 and K == 1 << info["l"]
+    assert E[0] == 0 and E[-1] == n
+    z = gen.zipf_u64(n, 12)
+    kmin = int(z.min())
+    assert orc.log_digit(int(z.max()) - kmin, M) < K <= 256
+    Ge = orc.elements(g, dtype)
+    Oe = orc.elements(orc.sort(a, dtype), dtype)
+    gk = (g if dtype != PAIR else g.reshape(-1, 2)[:, 0]).astype(np.uint64)
+    sizes = np.diff(E.astype(np.int64))
+    assert sizes.max() < n // 4  # the plain digit's bucket 0 holds > half of Zipf
+    for j in range(K):
+        e0, e1 = int(E[j]), int(E[j + 1])
+        for i in range(e0, e1, max(1, (e1 - e0) // 16)):
+            assert orc.log_digit(int(gk[i]) - kmin, M) == j
+        if e1 > e0:
+            assert orc.log_digit(int(gk[e1 - 1]) - kmin, M) == j
+            seg = orc.sort(np.ascontiguousarray(Ge[e0:e1]).reshape(-1), dtype)
+            assert orc.parity(seg, np.ascontiguousarray(Oe[e0:e1]).reshape(-1), dtype) == -1
+
+
+@pytest.mark.parametrize("dtype", [U64, F64, U32, PAIR])
+@pytest.mark.parametrize("n", [100003, 1 << 21, 5 * (1 << 20) + 17])
+def test_sort_digit_adaptive_zipf(ips, orc, dtype, n):
+    """Full IPS2Ra sorts of Zipf keys (adaptive extractor at the root, plain
+    digits below) against the oracle."""
+    a = make(dtype, n, 7, "zipf")
+    g, _ = gpu_sort(a, dtype, algo=ips.DIGIT)
+    check(orc, a, g, dtype)
+    g, _ = gpu_sort(a, dtype, algo=ips.DIGIT, base_cap=1024)
+    check(orc, a, g, dtype)
+
+
 # ----------------------------------------------------------------- full sorts
 SIZES = [0, 1, 2, 3, 31, 32, 33, 63, 64, 65, 4095, 4097, 24575, 24576, 24577, 49153, 100003]
 

@@ -549,3 +549,34 @@ def test_multiset_hash_and_is_sorted_reject_changes(orc, dtype):
         P = s.reshape(n, D).copy()
         P[n // 2, D - 1] ^= 1
         assert orc.parity(P.reshape(-1), s, dtype) != -1
+
+
+def test_log_digit_pins(orc):
+    """orc_log_digit (DESIGN R33) against what its definition fixes, none of it
+    through the oracle's own formula: the identity below 2^(M+1); brute force
+    over every offset below 2^14 that the mapping is monotone, hits every slot
+    (steps of 0 or 1), and gives every octave [2^e, 2^(e+1)), e > M, exactly
+    2^M slots of 2^(e-M) offsets each; hand-computed values; and the slot
+    count of a range, 2^M (bitlen(R) - M + 1) slots up to the octave of R."""
+    for M in range(1, 8):
+        prev = -1
+        per_slot = {}
+        for d in range(1 << 14):
+            q = orc.log_digit(d, M)
+            if d < (2 << M):
+                assert q == d
+            assert q - prev in (0, 1)
+            prev = q
+            per_slot[q] = per_slot.get(q, 0) + 1
+        for e in range(M + 1, 14):
+            slots = sorted({orc.log_digit(d, M) for d in range(1 << e, 2 << e)})
+            assert len(slots) == 1 << M
+            assert all(per_slot[q] == 1 << (e - M) for q in slots)
+    # by hand, M = 3: d = 16..31 is octave 4 (slot width 2): 16 -> 16, 17 -> 16,
+    # 30 -> 23; octave 5 (width 4) starts at slot 24: 32 -> 24, 63 -> 31;
+    # d = 2^40 opens octave 40: 8 * (40 - 3 + 1) = 304
+    assert [orc.log_digit(d, 3) for d in (15, 16, 17, 30, 31, 32, 35, 36, 63, 64)] == [15, 16, 16, 23, 23, 24, 24, 25, 31, 32]
+    assert orc.log_digit(1 << 40, 3) == 304
+    assert orc.log_digit((1 << 41) - 1, 3) == 311
+    # M = 1: two slots per octave; 2^63 opens the last octave: 2 * (63 - 1 + 1) = 126
+    assert orc.log_digit(1 << 63, 1) == 126 and orc.log_digit((1 << 64) - 1, 1) == 127
