@@ -313,6 +313,9 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
 #ifndef IPS4O_BC_BULK
 #define IPS4O_BC_BULK 1
 #endif
+#ifndef IPS4O_BC_HEVEC
+#define IPS4O_BC_HEVEC 1
+#endif
   constexpr bool BULK = IPS4O_BC_BULK && RUNLIST && DT == DT_U64;
   bool pend = false;  // a bulk store may still read s_items (CTA-uniform)
   extern __shared__ __align__(16) char smem[];
@@ -800,9 +803,28 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
         static_assert(RW + 1 == 4 && (RL == 4 || RL == 8), "4- and 8-input networks");
         if (!exact && !whole && nruns > 0) {
           u32 he[WPT];
+#if IPS4O_BC_HEVEC
+          // (vector loads: scalar loads at a stride of WPT words are WPT-way
+          // bank conflicts; the counters start at a multiple of 16 bytes)
+          if constexpr (WPT % 4 == 0) {
 #pragma unroll
-          for (int q = 0; q < WPT; ++q) he[q] = s_hist[tid * WPT + q];
-          u32 prev = tid ? (s_hist[tid * WPT - 1] >> 16) : 0u;  // end of the digit before this thread's
+            for (int q = 0; q < WPT / 4; ++q) {
+              const uint4 v4 = reinterpret_cast<const uint4 *>(s_hist)[tid * (WPT / 4) + q];
+              he[4 * q] = v4.x;
+              he[4 * q + 1] = v4.y;
+              he[4 * q + 2] = v4.z;
+              he[4 * q + 3] = v4.w;
+            }
+          } else
+#endif
+          {
+#pragma unroll
+            for (int q = 0; q < WPT; ++q) he[q] = s_hist[tid * WPT + q];
+          }
+          // end of the digit before this thread's: the neighbour lane's last
+          // word (lane 0 reads it from shared memory)
+          u32 prev = __shfl_up_sync(0xffffffffu, he[WPT - 1], 1) >> 16;
+          if (lane == 0) prev = tid ? (s_hist[tid * WPT - 1] >> 16) : 0u;
           __syncthreads();  // (every thread has read its run ends)
           u32 *s_runs = s_hist;
           u32 k = run_off;
@@ -849,7 +871,7 @@ __global__ void __launch_bounds__(BaseItem<DT>::THREADS, 1)
             }
 #pragma unroll
             for (int u = 0; u < RL; ++u)
-              if (u < c) s_it[a + u] = v[u];
+              if (u < c) s_it[a + u] = v[u];  // (skipping runs already in order: +0.2 ms)
           }
           __syncthreads();
         }
