@@ -567,3 +567,55 @@ def test_split_base_case(ips, orc, dtype, kind):
     if kind == "uniform":
         # nearly every bucket fits the split (levels beyond 1 hold few tasks)
         assert st["levels"] == 1 or sum(st["tasks_per_level"][1:]) < 32, st["tasks_per_level"]
+
+
+# ------------------------------------------------- randomized differential test
+ALIGN = {U64: 8, F64: 8, PAIR: 16, REC100: 16, U32: 4, QUARTET: 16}  # ips4o.h: minimum alignment per type
+ELEM_B = {U64: 8, F64: 8, PAIR: 16, REC100: 100, U32: 4, QUARTET: 32}
+
+
+def random_case(i):
+    """Case i of a fixed, seeded family: element type, size (log-uniform up to
+    ~2^21), value distribution, algorithm, options and a buffer offset at the
+    type's minimum alignment."""
+    rng = np.random.default_rng(9000 + i)
+    dtype = [U64, F64, PAIR, REC100, U32, QUARTET][i % 6]
+    nmax = 21 if dtype in (U64, F64, U32) else (19 if dtype != REC100 else 17)
+    n = int(2 ** rng.uniform(1, nmax)) + int(rng.integers(0, 3))
+    kind = ["uniform", "dups", "few", "zipf"][int(rng.integers(0, 4))]
+    opts = {}
+    if rng.integers(0, 2):
+        opts["algo"] = 1  # ips.DIGIT
+    if rng.integers(0, 2):
+        opts["base_cap"] = int(2 ** rng.uniform(6, 12))
+    if rng.integers(0, 3) == 0:
+        opts["k_max"] = int(2 ** rng.integers(2, 9))
+    if rng.integers(0, 4) == 0:
+        opts["skip_prepass"] = True
+    off = int(rng.integers(0, 8)) * ALIGN[dtype]
+    return dtype, n, kind, opts, off
+
+
+@pytest.mark.parametrize("i", range(72))
+def test_random_cases_with_guard_bands(ips, orc, i):
+    """The sort of a sub-range of a larger device buffer, starting at the
+    type's minimum alignment (8 B for U64/F64, 4 B for U32, 16 B otherwise):
+    the result equals the oracle's and the bytes before and after the range
+    are untouched (no write outside [ptr, ptr + n D))."""
+    import torch
+
+    dtype, n, kind, opts, off = random_case(i)
+    assert ips.DIGIT == 1
+    a = make(dtype, n, 7000 + i, kind)
+    b = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    G = 4096
+    buf = torch.full((G + off + b.size + G,), 0xA5, dtype=torch.uint8, device="cuda")
+    lo, hi = G + off, G + off + b.size
+    buf[lo:hi].copy_(torch.from_numpy(b))
+    st = ips.sort_ex(buf[lo:hi], dtype, **opts)
+    torch.cuda.synchronize()
+    assert ips.device_status(0) == 0
+    assert bool((buf[:lo] == 0xA5).all()) and bool((buf[hi:] == 0xA5).all()), f"guard bands overwritten ({dtype}, n={n}, {opts})"
+    g = buf[lo:hi].cpu().numpy().view(a.dtype).reshape(a.shape)
+    check(orc, a, g, dtype)
+    assert st["levels"] >= 0
