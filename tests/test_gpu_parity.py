@@ -596,7 +596,7 @@ def random_case(i):
     return dtype, n, kind, opts, off
 
 
-@pytest.mark.parametrize("i", range(72))
+@pytest.mark.parametrize("i", range(240))
 def test_random_cases_with_guard_bands(ips, orc, i):
     """The sort of a sub-range of a larger device buffer, starting at the
     type's minimum alignment (8 B for U64/F64, 4 B for U32, 16 B otherwise):
