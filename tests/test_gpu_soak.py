@@ -25,16 +25,17 @@ from test_gpu_parity import check, ips, make, random_case  # noqa: F401  (ips: f
 pytestmark = pytest.mark.gpu
 
 SOAK_S = float(os.environ.get("IPS4O_SOAK_SECONDS", "0"))
+START = int(os.environ.get("IPS4O_SOAK_START", "240"))  # first random case / seed offset of a run
 needs_soak = pytest.mark.skipif(SOAK_S <= 0, reason="opt-in: set IPS4O_SOAK_SECONDS")
 
 
 @needs_soak
 def test_soak_random_cases(ips, orc):
-    """Random cases 240, 241, ... for half of the soak time."""
+    """Random cases START, START + 1, ... (default 240) for half of the soak time."""
     import torch
 
     t_end = time.time() + SOAK_S / 2
-    i = 240
+    i = START
     while time.time() < t_end:
         dtype, n, kind, opts, off = random_case(i)
         a = make(dtype, n, 7000 + i, kind)
@@ -50,7 +51,7 @@ def test_soak_random_cases(ips, orc):
         g = buf[lo:hi].cpu().numpy().view(a.dtype).reshape(a.shape)
         check(orc, a, g, dtype)
         i += 1
-    print(f"soak: random cases 240..{i - 1} pass", flush=True)
+    print(f"soak: random cases {START}..{i - 1} pass", flush=True)
 
 
 def _ordered_i64(t, dtype):
@@ -82,11 +83,12 @@ def test_soak_large_sorts(ips):
 
     t_end = time.time() + SOAK_S / 2
     it = 0
+    sh = START % 7  # another run pairs sizes and distributions differently
     while time.time() < t_end:
         dtype, dist = BIG[it % len(BIG)]
-        lg = [30, 26, 28, 27, 29][it % 5]
+        lg = [30, 26, 28, 27, 29][(it + sh) % 5]
         n = (1 << lg) - (it * 977) % 4099
-        a = getattr(gen, dist)(n, 500 + it)
+        a = getattr(gen, dist)(n, 260 + START + it)
         t = torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1)).cuda()
         want = torch.sort(_ordered_i64(t, dtype)).values
         for rep in range(4):  # the same input again (twice per algorithm): the interleavings differ
