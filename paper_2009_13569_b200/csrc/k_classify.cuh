@@ -593,6 +593,20 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
     //      blocks are [boff_j, boff_j + nb_j): block 0 from buffer j, the
     //      rest from the stage.  One warp per block.
     {
+#ifndef IPS4O_CLS_COPY_WARP
+#define IPS4O_CLS_COPY_WARP 0
+#endif
+#if IPS4O_CLS_COPY_WARP
+      for (u32 g = wid; g < nblocks; g += NWARPS) {  // a block per warp: 2 x 256 contiguous bytes
+        const u32 jq = s_blkb[g];
+        const u32 j = jq & 0x1FFu, q = jq >> 9;
+        const Unit *src = q == 0 ? s_buf + j * BUFS : s_stage + ((s_plan[j] >> 21) + q - 1) * B;
+        Unit *dst = gtask + s0 + (front + g) * B;
+        if (!IPS4O_GUARD(s0 + (front + g + 1) * B <= s1, A.err)) continue;  // blocks stay in the stripe
+#pragma unroll
+        for (int e = 0; e < B / 32; ++e) dst[lane + 32 * e] = src[lane + 32 * e];
+      }
+#else
       const u32 half = (u32)lane >> 4, hl = (u32)lane & 15u;
       for (u32 g = 2 * wid + half; g < nblocks; g += 2 * NWARPS) {  // a block per half-warp
         const u32 jq = s_blkb[g];
@@ -603,6 +617,7 @@ __global__ void __launch_bounds__(ClsV2<DT>::NT, 1) classify_v2_kernel(LevelArgs
 #pragma unroll
         for (int e = 0; e < B / 16; ++e) dst[hl + 16 * e] = src[hl + 16 * e];
       }
+#endif
       // the buckets of the emitted blocks, for K4 (coalesced 2-byte stores by
       // the last warp; warp 0 issues the prefetches)
       if (wid == NWARPS - 1) {
